@@ -1,0 +1,147 @@
+/*
+ * idkit_b200.h -- C ABI of the B200-native interpolative-decomposition path.
+ *
+ * Drop-in boundary for the reference library idkit (/root/reference/proj).
+ * The reference's boundary is a C++ API (include/idkit/*.hpp) with value
+ * semantics and exceptions; this header is the extern "C" layer beneath a
+ * C++ shim that keeps those signatures.  Every entry
+ * names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Matrices are column-major fp64 with an explicit leading dimension, the
+ *     idkit::Matrix storage contract ((i,j) at data[j*ld+i], matrix.hpp:34-35).
+ *   - Indices are int64_t (the reference uses std::size_t).
+ *   - `d_` pointers are device memory (cudaMalloc / torch CUDA tensors);
+ *     `h_` pointers are host memory (pinned or pageable).
+ *   - Every call is stream-ordered on the handle's stream.  Entries that
+ *     must report a data-dependent error (singular R11) synchronise that
+ *     stream before returning, exactly like the reference returns or throws.
+ *   - Status codes map one-to-one to the reference's exception types
+ *     (errors.hpp:9-41, std::invalid_argument); the message of the last
+ *     failure is kept per handle.  Handles are not shared between threads;
+ *     concurrent calls on distinct handles are safe.
+ *   - There is no CPU fallback: without a usable sm_100 device every call
+ *     returns IDK_ERR_CUDA.
+ */
+#ifndef IDKIT_B200_H
+#define IDKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IDK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define IDK_API __attribute__((visibility("default")))
+#else
+#define IDK_API
+#endif
+
+typedef struct idk_context* idk_handle;
+
+typedef enum {
+    IDK_OK = 0,
+    IDK_ERR_INVALID_ARG = 1,  /* std::invalid_argument (id.cpp:14-18, 50-51; qr.cpp:45-46) */
+    IDK_ERR_SINGULAR = 2,     /* idkit::SingularMatrixError (solve.cpp:27-30)              */
+    IDK_ERR_NOT_POSDEF = 3,   /* idkit::NotPositiveDefiniteError (solve.cpp:66-68)         */
+    IDK_ERR_CUDA = 4,         /* CUDA runtime failure / no sm_100 device                   */
+    IDK_ERR_NO_MEMORY = 5,    /* device allocation failed                                  */
+    IDK_ERR_NCCL = 6          /* reserved for the sharded host layer                       */
+} idk_status;
+
+/* How the Gaussian sketch Omega (l x m) is produced. */
+typedef enum {
+    IDK_OMEGA_PHILOX = 0,   /* on device: Philox4x32-10(seed, element index) + Box-Muller */
+    IDK_OMEGA_MT19937 = 1,  /* on host: the reference's generate(gaussian, l, m, seed)
+                               stream (datasets.cpp:15-33, mt19937_64), then uploaded      */
+    IDK_OMEGA_VERBATIM = 2  /* caller-provided d_omega (l x m, ld = l)                     */
+} idk_omega_mode;
+
+/* ---- handle ---------------------------------------------------------------- */
+IDK_API int idk_abi_version(void);
+IDK_API int idk_create(idk_handle* out, int device);
+IDK_API int idk_destroy(idk_handle h);
+/* cudaStream_t passed as void*; NULL = the legacy default stream. */
+IDK_API int idk_set_stream(idk_handle h, void* stream);
+IDK_API const char* idk_last_error(idk_handle h);
+IDK_API const char* idk_status_string(int status);
+/* Number of kernels this handle launched since creation (bench evidence). */
+IDK_API int64_t idk_kernel_launches(idk_handle h);
+
+/* ---- the ID path (device pointers) ----------------------------------------- */
+
+/* Deterministic rank-k ID of A (m x n, lda).  Replaces idkit::optim_id
+ * (id.hpp:40, id.cpp:29-45): cols = first k pivots of qr_column_pivoted(A, k);
+ * Z = [I | R11^-1 R12] P^T (k x n, ld = k) -- equal to the reference's
+ * normal-equation Z in exact arithmetic; C = A[:, cols] (m x k, ld = m) if
+ * d_c != NULL.  Rank deficiency (zero |r_ii|) -> IDK_ERR_NOT_POSDEF, as the
+ * reference's Cholesky raises (test_id.cpp:120-129). */
+IDK_API int idk_optim_id(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k,
+                 int64_t* d_cols, double* d_z, double* d_c);
+
+/* Gaussian-sketch randomized ID (the north-star RID): Y = Omega * M with
+ * Omega (k+p) x m, CPQR(Y, k), Z = [I | R11^-1 R12] P^T, C = M[:, cols].
+ * M is A (m x n, lda >= m) or, when a_transposed != 0, the transpose of the
+ * stored n x m matrix A (lda >= n) -- the id_auto dual (id.cpp:78-95) without
+ * materialising A^T.  Then C (m x k) holds rows of the stored matrix.
+ * Composed reference: generate -> matmul -> qr_column_pivoted ->
+ * solve_triangular -> select_columns.  A zero |r_ii| ->
+ * IDK_ERR_SINGULAR (solve.cpp:27-30). */
+IDK_API int idk_sketch_rid(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int a_transposed,
+                   int64_t k, int64_t p, uint64_t seed, int omega_mode, const double* d_omega,
+                   int64_t* d_cols, double* d_z, double* d_c);
+
+/* Orientation dispatch, idkit::id_auto (id.hpp:55-56, id.cpp:78-95): A is
+ * m x n; if m <= n the ID runs on A, else on A^T with *transposed = 1, cols
+ * indexing rows of A and Z being k x m.  method 0 = deterministic
+ * (idk_optim_id), 1 = Gaussian-sketch RID (idk_sketch_rid).  d_z must hold
+ * k * max(m, n) doubles; d_c (optional) m x k or n x k accordingly. */
+IDK_API int idk_id_auto(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int method,
+                uint64_t seed, int64_t p, int omega_mode, const double* d_omega, int64_t* d_cols,
+                double* d_z, double* d_c, int* transposed);
+
+/* Batched deterministic ID (BASELINE cfg3): batch independent m x n
+ * matrices at d_a + b*stride (lda each), one CTA per matrix, outputs packed:
+ * cols b*k, Z b*k*n, C b*m*k.  Bit-identical to the reference composition
+ * qr_column_pivoted -> solve_triangular -> select_columns per matrix.
+ * Needs m*n small enough for shared memory (64 x 256 uses 139 KB).  A zero
+ * |r_ii| in any matrix -> IDK_ERR_NOT_POSDEF (first failing batch index in
+ * the message). */
+IDK_API int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t m, int64_t n, int64_t lda,
+                         int64_t stride, int64_t k, int64_t* d_cols, double* d_z, double* d_c);
+
+/* ---- stages / primitives (device pointers) ---------------------------------- */
+
+/* Omega (l x m, ld = l) = Philox Gaussian, keyed by seed (mirrors idko_omega_philox). */
+IDK_API int idk_sketch_omega(idk_handle h, int64_t l, int64_t m, uint64_t seed, double* d_omega);
+
+/* Y (l x n, ldy) = Omega (l x m, ld = l) * M, M = A or A^T as in idk_sketch_rid.
+ * Replaces matmul(Omega, A) (matrix.cpp:28-48) on the DMMA pipe. */
+IDK_API int idk_sketch(idk_handle h, const double* d_omega, int64_t l, const double* d_a, int64_t m, int64_t n,
+               int64_t lda, int a_transposed, double* d_y, int64_t ldy);
+
+/* idkit::qr_column_pivoted (qr.hpp:34, qr.cpp:42-126): q (m x steps, may be
+ * NULL), r (steps x n, may be NULL), perm (n, may be NULL).  d_work (m x n,
+ * ld = m) receives the factored matrix if not NULL. */
+IDK_API int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t steps,
+                          double* d_q, double* d_r, int64_t* d_perm);
+
+/* idkit::select_columns (matrix.hpp:76, matrix.cpp:121-130): out (m x ncols)
+ * = A[:, cols]; rows_of_a != 0 gathers rows instead (out is n x ncols). */
+IDK_API int idk_select_columns(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, const int64_t* d_cols,
+                       int64_t ncols, int rows_of_a, double* d_out);
+
+/* ---- host-buffer entries (the reference's value-semantics calls) ------------ */
+
+/* Same as idk_id_auto, host pointers in and out; host<->device copies are
+ * part of the call.  h_a is m x n (ld = m); h_z holds k * max(m, n). */
+IDK_API int idk_id_auto_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int method, uint64_t seed,
+                     int64_t p, int omega_mode, int64_t* h_cols, double* h_z, double* h_c, int* transposed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,19 @@
+"""paper_2105_07076_b200 -- B200-native interpolative decomposition (ID) path.
+
+Drop-in for the hot path of the reference library idkit (arXiv 2105.07076,
+"Optim ID / Optim RID"): Gaussian sketch -> column-pivoted Householder QR ->
+Z = [I | R11^-1 R12] P^T -> C = A[:, cols], as hand-written sm_100a kernels
+behind the C ABI in include/idkit_b200.h.  `idkit` is the Python mirror of the
+reference's C++ API; `sharded` is the multi-GPU (torch.distributed) layer.
+"""
+from .idkit import (DETERMINISTIC, OMEGA_MT19937, OMEGA_PHILOX, OMEGA_VERBATIM, RANDOMIZED, Context, CudaError,
+                    IdkitError, IdResult, InvalidArgument, NotPositiveDefiniteError, PivotedQr, SingularMatrixError,
+                    context, id_auto, optim_id, optim_id_batched, qr_column_pivoted, select_columns, sketch,
+                    sketch_omega, sketch_rid)
+
+__all__ = [
+    "DETERMINISTIC", "RANDOMIZED", "OMEGA_PHILOX", "OMEGA_MT19937", "OMEGA_VERBATIM", "Context", "CudaError",
+    "IdkitError", "IdResult", "InvalidArgument", "NotPositiveDefiniteError", "PivotedQr", "SingularMatrixError",
+    "context", "id_auto", "optim_id", "optim_id_batched", "qr_column_pivoted", "select_columns", "sketch",
+    "sketch_omega", "sketch_rid",
+]

@@ -1,0 +1,478 @@
+// capi.cu -- the extern "C" boundary (include/idkit_b200.h) and the host-side
+// orchestration of the ID path on one B200.
+//
+// Stage order per call (all on the handle's stream):
+//   sketch RID : [Omega] -> DMMA GEMM Y = Omega M -> persistent CPQR(Y, k)
+//                -> R11 gather + blocked TRSM writing Z -> C gather -> status
+//   det ID     : copy (or transpose) A -> persistent CPQR(A, k) -> same tail
+//   batched    : one fused kernel, one CTA per matrix
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/idkit_b200.h"
+#include "kernels.h"
+
+struct idk_context {
+    int device = 0;
+    int num_sms = 0;
+    size_t smem_optin = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    // compute workspace (bump-allocated per call, grow-only)
+    char* ws = nullptr;
+    size_t ws_cap = 0;
+    size_t ws_off = 0;
+    // host-entry staging (device copies of host inputs/outputs)
+    char* io = nullptr;
+    size_t io_cap = 0;
+    int* h_status = nullptr;  // pinned
+    double* h_omega = nullptr;  // pinned staging for IDK_OMEGA_MT19937
+    size_t h_omega_cap = 0;
+    int64_t launches = 0;
+};
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+int set_err(idk_context* h, int code, const std::string& msg) {
+    if (h) h->err = msg;
+    return code;
+}
+
+int cuda_fail(idk_context* h, cudaError_t e, const char* where) {
+    return set_err(h, IDK_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define IDK_CUDA(call)                                      \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) return cuda_fail(h, _e, #call); \
+    } while (0)
+
+// Grow-only buffer; growing synchronises the stream first (callers never
+// hold pointers across calls: every entry synchronises before returning).
+int ensure(idk_context* h, char** buf, size_t* cap, size_t bytes) {
+    if (bytes <= *cap) return IDK_OK;
+    cudaStreamSynchronize(h->stream);
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    size_t want = std::max(bytes, static_cast<size_t>(1) << 20);
+    if (cudaMalloc(reinterpret_cast<void**>(buf), want) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(h, IDK_ERR_NO_MEMORY, "cudaMalloc of " + std::to_string(want) + " bytes failed");
+    }
+    *cap = want;
+    return IDK_OK;
+}
+
+struct Carve {
+    size_t total = 0;
+    size_t take(size_t bytes) {
+        const size_t off = total;
+        total += align_up(bytes);
+        return off;
+    }
+};
+
+int check_k(idk_context* h, int64_t m, int64_t n, int64_t k, const char* op) {
+    if (m <= 0 || n <= 0) return set_err(h, IDK_ERR_INVALID_ARG, std::string(op) + ": empty matrix");
+    if (k < 1 || k > std::min(m, n))
+        return set_err(h, IDK_ERR_INVALID_ARG, std::string(op) + ": k must lie in [1, min(rows, cols)]");
+    if (k > INT_MAX || m > INT_MAX) return set_err(h, IDK_ERR_INVALID_ARG, std::string(op) + ": dimension too large");
+    return IDK_OK;
+}
+
+// Largest co-resident grid for the persistent CPQR kernel.
+int cpqr_ctas(idk_context* h) { return h->num_sms; }
+
+// Work buffers of one CPQR + Z solve on an m' x n matrix.
+struct CpqrWs {
+    size_t pos, pivots, taus, pub, barrier, r11, status;
+};
+
+CpqrWs carve_cpqr(Carve& cv, int64_t n, int64_t k, int num_sms) {
+    CpqrWs w;
+    w.pos = cv.take(sizeof(long long) * n);
+    w.pivots = cv.take(sizeof(long long) * k);
+    w.taus = cv.take(sizeof(double) * k);
+    w.pub = cv.take(idk::kCpqrPubBytes * 3 * static_cast<size_t>(num_sms + 1));
+    w.barrier = cv.take(sizeof(unsigned));
+    w.r11 = cv.take(sizeof(double) * k * k);
+    w.status = cv.take(sizeof(int));
+    return w;
+}
+
+int check_cpqr_fits(idk_context* h, int64_t mrows, int64_t n) {
+    const int64_t G = std::min<int64_t>(n, h->num_sms);
+    const int cols = static_cast<int>((n + G - 1) / G);
+    if (idk::cpqr_smem_bytes(static_cast<int>(mrows), cols) > 200 * 1024)
+        return set_err(h, IDK_ERR_INVALID_ARG,
+                       "qr_column_pivoted: " + std::to_string(mrows) + " rows x " + std::to_string(n) +
+                           " columns exceeds the persistent CPQR shared-memory budget");
+    return IDK_OK;
+}
+
+// CPQR(W) -> Z, C, cols; W is m' x n (ld m'), already resident and mutable.
+int factor_and_solve(idk_context* h, double* W, int64_t mrows, int64_t n, int64_t k, char* base, const CpqrWs& w,
+                     const double* d_a, int64_t lda, int64_t m_out, bool rows_of_a, int64_t* d_cols, double* d_z,
+                     double* d_c, bool det) {
+    long long* pos = reinterpret_cast<long long*>(base + w.pos);
+    long long* piv = reinterpret_cast<long long*>(base + w.pivots);
+    double* taus = reinterpret_cast<double*>(base + w.taus);
+    int* status = reinterpret_cast<int*>(base + w.status);
+    IDK_CUDA(idk::cpqr_launch(W, mrows, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
+                              reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream));
+    IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
+    IDK_CUDA(idk::id_solve_z(W, mrows, static_cast<int>(k), n, piv, pos, reinterpret_cast<double*>(base + w.r11),
+                             status, d_z, h->stream));
+    h->launches += 3;
+    if (d_c) {
+        IDK_CUDA(idk::gather_columns(d_a, lda, m_out, piv, static_cast<int>(k), rows_of_a, d_c, h->stream));
+        h->launches += 1;
+    }
+    IDK_CUDA(cudaMemcpyAsync(d_cols, piv, sizeof(long long) * k, cudaMemcpyDeviceToDevice, h->stream));
+    IDK_CUDA(cudaMemcpyAsync(h->h_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    const int bad = *h->h_status;
+    if (bad != 0x7f7f7f7f) {
+        if (det)
+            return set_err(h, IDK_ERR_NOT_POSDEF,
+                           "optim_id: rank-deficient input (R11 diagonal " + std::to_string(bad) +
+                               " is zero; reference: solve_posdef non-positive pivot)");
+        return set_err(h, IDK_ERR_SINGULAR, "solve_triangular: zero diagonal at index " + std::to_string(bad));
+    }
+    return IDK_OK;
+}
+
+// Deterministic ID of M (m x n).  M = A (lda >= m) or A^T (A stored n x m, lda >= n).
+int det_id(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda, bool trans, int64_t k,
+           int64_t* d_cols, double* d_z, double* d_c) {
+    int rc = check_k(h, m, n, k, "optim_id");
+    if (rc) return rc;
+    if (!d_a || !d_cols || !d_z) return set_err(h, IDK_ERR_INVALID_ARG, "optim_id: null pointer");
+    if (lda < (trans ? n : m)) return set_err(h, IDK_ERR_INVALID_ARG, "optim_id: lda too small");
+    if ((rc = check_cpqr_fits(h, m, n))) return rc;
+    Carve cv;
+    const size_t wofs = cv.take(sizeof(double) * m * n);
+    const CpqrWs w = carve_cpqr(cv, n, k, h->num_sms);
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    double* W = reinterpret_cast<double*>(h->ws + wofs);
+    if (trans) {
+        IDK_CUDA(idk::transpose_copy(d_a, lda, n, m, W, m, h->stream));
+        h->launches += 1;
+    } else {
+        IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
+                                   cudaMemcpyDeviceToDevice, h->stream));
+    }
+    return factor_and_solve(h, W, m, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, true);
+}
+
+// Reference Box-Muller over mt19937_64 (random.cpp:10-15), column-major fill
+// like generate(gaussian, l, m, seed) (datasets.cpp:15-33).
+void host_generate_gaussian(double* out, int64_t total, uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    const double two_pi = 2.0 * 3.141592653589793238462643383279502884;
+    for (int64_t e = 0; e < total; ++e) {
+        const double u1 = static_cast<double>((rng() >> 11) + 1) * 0x1.0p-53;
+        const double u2 = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+        out[e] = std::sqrt(-2.0 * std::log(u1)) * std::cos(two_pi * u2);
+    }
+}
+
+int sketch_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda, bool trans, int64_t k,
+               int64_t p, uint64_t seed, int omega_mode, const double* d_omega, int64_t* d_cols, double* d_z,
+               double* d_c) {
+    int rc = check_k(h, m, n, k, "sketch_rid");
+    if (rc) return rc;
+    if (p < 0) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: oversampling p must be non-negative");
+    if (!d_a || !d_cols || !d_z) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: null pointer");
+    if (lda < (trans ? n : m)) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: lda too small");
+    if (omega_mode < 0 || omega_mode > 2) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: bad omega mode");
+    if (omega_mode == IDK_OMEGA_VERBATIM && !d_omega)
+        return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: verbatim omega requires d_omega");
+    const int64_t l = k + p;
+    if ((rc = check_cpqr_fits(h, l, n))) return rc;
+    const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(l), n, m, h->num_sms);
+    Carve cv;
+    const size_t oofs = omega_mode == IDK_OMEGA_VERBATIM ? 0 : cv.take(sizeof(double) * l * m);
+    const size_t yofs = cv.take(sizeof(double) * l * n);
+    const size_t pofs = splits > 1 ? cv.take(sizeof(double) * l * n * splits) : 0;
+    const CpqrWs w = carve_cpqr(cv, n, k, h->num_sms);
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    const double* omega = d_omega;
+    if (omega_mode != IDK_OMEGA_VERBATIM) {
+        double* om = reinterpret_cast<double*>(h->ws + oofs);
+        if (omega_mode == IDK_OMEGA_PHILOX) {
+            IDK_CUDA(idk::omega_philox(om, l, m, seed, h->stream));
+            h->launches += 1;
+        } else {
+            const size_t bytes = sizeof(double) * l * m;
+            if (bytes > h->h_omega_cap) {
+                cudaStreamSynchronize(h->stream);
+                if (h->h_omega) cudaFreeHost(h->h_omega);
+                h->h_omega = nullptr;
+                h->h_omega_cap = 0;
+                IDK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->h_omega), bytes));
+                h->h_omega_cap = bytes;
+            }
+            IDK_CUDA(cudaStreamSynchronize(h->stream));  // staging buffer may still be in flight
+            host_generate_gaussian(h->h_omega, l * m, seed);
+            IDK_CUDA(cudaMemcpyAsync(om, h->h_omega, bytes, cudaMemcpyHostToDevice, h->stream));
+        }
+        omega = om;
+    }
+    double* Y = reinterpret_cast<double*>(h->ws + yofs);
+    IDK_CUDA(idk::sketch_gemm(omega, l, d_a, lda, trans, Y, l, static_cast<int>(l), n, m, splits,
+                              splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr, h->stream));
+    h->launches += splits > 1 ? 2 : 1;
+    return factor_and_solve(h, Y, l, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, false);
+}
+
+int id_auto_dev(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int method,
+                uint64_t seed, int64_t p, int omega_mode, const double* d_omega, int64_t* d_cols, double* d_z,
+                double* d_c, int* transposed) {
+    int rc = check_k(h, m, n, k, "id_auto");
+    if (rc) return rc;
+    if (method != 0 && method != 1) return set_err(h, IDK_ERR_INVALID_ARG, "id_auto: method must be 0 or 1");
+    const bool tall = m > n;
+    if (transposed) *transposed = tall ? 1 : 0;
+    if (!tall) {
+        return method == 0 ? det_id(h, d_a, m, n, lda, false, k, d_cols, d_z, d_c)
+                           : sketch_rid(h, d_a, m, n, lda, false, k, p, seed, omega_mode, d_omega, d_cols, d_z, d_c);
+    }
+    // Dual: decompose M = A^T (n x m), stored as A (m x n, lda >= m).
+    return method == 0 ? det_id(h, d_a, n, m, lda, true, k, d_cols, d_z, d_c)
+                       : sketch_rid(h, d_a, n, m, lda, true, k, p, seed, omega_mode, d_omega, d_cols, d_z, d_c);
+}
+
+}  // namespace
+
+extern "C" {
+
+int idk_abi_version(void) { return IDK_ABI_VERSION; }
+
+const char* idk_status_string(int status) {
+    switch (status) {
+        case IDK_OK: return "ok";
+        case IDK_ERR_INVALID_ARG: return "invalid argument";
+        case IDK_ERR_SINGULAR: return "singular matrix";
+        case IDK_ERR_NOT_POSDEF: return "not positive definite";
+        case IDK_ERR_CUDA: return "cuda error";
+        case IDK_ERR_NO_MEMORY: return "out of device memory";
+        case IDK_ERR_NCCL: return "nccl error";
+        default: return "unknown status";
+    }
+}
+
+int idk_create(idk_handle* out, int device) {
+    if (!out) return IDK_ERR_INVALID_ARG;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return IDK_ERR_CUDA;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) return IDK_ERR_CUDA;
+    if (cudaSetDevice(device) != cudaSuccess) return IDK_ERR_CUDA;
+    idk_context* h = new idk_context();
+    h->device = device;
+    h->num_sms = prop.multiProcessorCount;
+    h->smem_optin = prop.sharedMemPerBlockOptin;
+    if (cudaMallocHost(reinterpret_cast<void**>(&h->h_status), sizeof(int) * 4) != cudaSuccess) {
+        delete h;
+        return IDK_ERR_CUDA;
+    }
+    *out = h;
+    return IDK_OK;
+}
+
+int idk_destroy(idk_handle h) {
+    if (!h) return IDK_OK;
+    cudaStreamSynchronize(h->stream);
+    if (h->ws) cudaFree(h->ws);
+    if (h->io) cudaFree(h->io);
+    if (h->h_status) cudaFreeHost(h->h_status);
+    if (h->h_omega) cudaFreeHost(h->h_omega);
+    delete h;
+    return IDK_OK;
+}
+
+int idk_set_stream(idk_handle h, void* stream) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    h->stream = static_cast<cudaStream_t>(stream);
+    return IDK_OK;
+}
+
+const char* idk_last_error(idk_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+int64_t idk_kernel_launches(idk_handle h) { return h ? h->launches : 0; }
+
+int idk_optim_id(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int64_t* d_cols,
+                 double* d_z, double* d_c) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    return det_id(h, d_a, m, n, lda, false, k, d_cols, d_z, d_c);
+}
+
+int idk_sketch_rid(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int a_transposed, int64_t k,
+                   int64_t p, uint64_t seed, int omega_mode, const double* d_omega, int64_t* d_cols, double* d_z,
+                   double* d_c) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    return sketch_rid(h, d_a, m, n, lda, a_transposed != 0, k, p, seed, omega_mode, d_omega, d_cols, d_z, d_c);
+}
+
+int idk_id_auto(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int method,
+                uint64_t seed, int64_t p, int omega_mode, const double* d_omega, int64_t* d_cols, double* d_z,
+                double* d_c, int* transposed) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    return id_auto_dev(h, d_a, m, n, lda, k, method, seed, p, omega_mode, d_omega, d_cols, d_z, d_c, transposed);
+}
+
+int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t m, int64_t n, int64_t lda,
+                         int64_t stride, int64_t k, int64_t* d_cols, double* d_z, double* d_c) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (batch < 0) return set_err(h, IDK_ERR_INVALID_ARG, "optim_id_batched: negative batch");
+    int rc = check_k(h, m, n, k, "optim_id_batched");
+    if (rc) return rc;
+    if (lda < m || stride < lda * n) return set_err(h, IDK_ERR_INVALID_ARG, "optim_id_batched: bad lda/stride");
+    if (idk::batched_id_smem_bytes(static_cast<int>(m), static_cast<int>(n)) > h->smem_optin)
+        return set_err(h, IDK_ERR_INVALID_ARG, "optim_id_batched: m x n too large for one CTA's shared memory");
+    if (batch == 0) return IDK_OK;
+    Carve cv;
+    const size_t sofs = cv.take(sizeof(int) * batch);
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    int* status = reinterpret_cast<int*>(h->ws + sofs);
+    IDK_CUDA(idk::batched_id(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                             reinterpret_cast<long long*>(d_cols), d_z, d_c, status, h->stream));
+    h->launches += 1;
+    std::vector<int> st(static_cast<size_t>(batch));
+    IDK_CUDA(cudaMemcpyAsync(st.data(), status, sizeof(int) * batch, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    for (int64_t b = 0; b < batch; ++b)
+        if (st[b] >= 0)
+            return set_err(h, IDK_ERR_NOT_POSDEF, "optim_id_batched: matrix " + std::to_string(b) +
+                                                      " is rank deficient (R11 diagonal " + std::to_string(st[b]) +
+                                                      " is zero)");
+    return IDK_OK;
+}
+
+int idk_sketch_omega(idk_handle h, int64_t l, int64_t m, uint64_t seed, double* d_omega) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    if (l < 0 || m < 0 || (!d_omega && l * m > 0)) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_omega: bad args");
+    cudaSetDevice(h->device);
+    IDK_CUDA(idk::omega_philox(d_omega, l, m, seed, h->stream));
+    h->launches += 1;
+    return IDK_OK;
+}
+
+int idk_sketch(idk_handle h, const double* d_omega, int64_t l, const double* d_a, int64_t m, int64_t n, int64_t lda,
+               int a_transposed, double* d_y, int64_t ldy) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (l <= 0 || m <= 0 || n <= 0 || l > INT_MAX) return set_err(h, IDK_ERR_INVALID_ARG, "sketch: bad dimensions");
+    if (lda < (a_transposed ? n : m) || ldy < l) return set_err(h, IDK_ERR_INVALID_ARG, "sketch: bad leading dimension");
+    const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(l), n, m, h->num_sms);
+    int rc;
+    if (splits > 1 && (rc = ensure(h, &h->ws, &h->ws_cap, sizeof(double) * ldy * n * splits))) return rc;
+    IDK_CUDA(idk::sketch_gemm(d_omega, l, d_a, lda, a_transposed != 0, d_y, ldy, static_cast<int>(l), n, m, splits,
+                              reinterpret_cast<double*>(h->ws), h->stream));
+    h->launches += splits > 1 ? 2 : 1;
+    return IDK_OK;
+}
+
+int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t steps,
+                          double* d_q, double* d_r, int64_t* d_perm) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (m <= 0 || n <= 0 || steps < 1 || steps > std::min(m, n))
+        return set_err(h, IDK_ERR_INVALID_ARG, "qr_column_pivoted: max_steps must lie in [1, min(rows, cols)]");
+    if (lda < m) return set_err(h, IDK_ERR_INVALID_ARG, "qr_column_pivoted: lda too small");
+    int rc = check_cpqr_fits(h, m, n);
+    if (rc) return rc;
+    Carve cv;
+    const size_t wofs = cv.take(sizeof(double) * m * n);
+    const size_t permofs = cv.take(sizeof(long long) * n);
+    const CpqrWs w = carve_cpqr(cv, n, steps, h->num_sms);
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    char* base = h->ws;
+    double* W = reinterpret_cast<double*>(base + wofs);
+    IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
+                               cudaMemcpyDeviceToDevice, h->stream));
+    long long* pos = reinterpret_cast<long long*>(base + w.pos);
+    long long* piv = reinterpret_cast<long long*>(base + w.pivots);
+    double* taus = reinterpret_cast<double*>(base + w.taus);
+    IDK_CUDA(idk::cpqr_launch(W, m, static_cast<int>(m), n, static_cast<int>(steps), pos, piv, taus, base + w.pub,
+                              reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream));
+    long long* perm = d_perm ? reinterpret_cast<long long*>(d_perm) : reinterpret_cast<long long*>(base + permofs);
+    IDK_CUDA(idk::cpqr_finish(W, m, static_cast<int>(m), n, static_cast<int>(steps), pos, piv, taus, perm, d_r, d_q,
+                              h->stream));
+    h->launches += 1 + 1 + (d_r ? 1 : 0) + (d_q ? 1 : 0);
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    return IDK_OK;
+}
+
+int idk_select_columns(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, const int64_t* d_cols,
+                       int64_t ncols, int rows_of_a, double* d_out) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (m < 0 || n < 0 || ncols < 0 || lda < m) return set_err(h, IDK_ERR_INVALID_ARG, "select_columns: bad dimensions");
+    if (ncols == 0) return IDK_OK;
+    std::vector<int64_t> cols(static_cast<size_t>(ncols));
+    IDK_CUDA(cudaMemcpyAsync(cols.data(), d_cols, sizeof(int64_t) * ncols, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    const int64_t limit = rows_of_a ? m : n;
+    for (int64_t c : cols)
+        if (c < 0 || c >= limit) return set_err(h, IDK_ERR_INVALID_ARG, "select_columns: index out of range");
+    IDK_CUDA(idk::gather_columns(d_a, lda, rows_of_a ? n : m, reinterpret_cast<const long long*>(d_cols),
+                                 static_cast<int>(ncols), rows_of_a != 0, d_out, h->stream));
+    h->launches += 1;
+    return IDK_OK;
+}
+
+int idk_id_auto_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int method, uint64_t seed,
+                     int64_t p, int omega_mode, int64_t* h_cols, double* h_z, double* h_c, int* transposed) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    int rc = check_k(h, m, n, k, "id_auto");
+    if (rc) return rc;
+    if (!h_a || !h_cols || !h_z) return set_err(h, IDK_ERR_INVALID_ARG, "id_auto: null pointer");
+    if (omega_mode == IDK_OMEGA_VERBATIM)
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_auto_host: verbatim omega needs the device entry");
+    const bool tall = m > n;
+    const int64_t zc = tall ? m : n;
+    const int64_t crow = tall ? n : m;
+    Carve cv;
+    const size_t aofs = cv.take(sizeof(double) * m * n);
+    const size_t cofs = cv.take(sizeof(int64_t) * k);
+    const size_t zofs = cv.take(sizeof(double) * k * zc);
+    const size_t ccofs = cv.take(sizeof(double) * crow * k);
+    if ((rc = ensure(h, &h->io, &h->io_cap, cv.total))) return rc;
+    double* d_a = reinterpret_cast<double*>(h->io + aofs);
+    int64_t* d_cols = reinterpret_cast<int64_t*>(h->io + cofs);
+    double* d_z = reinterpret_cast<double*>(h->io + zofs);
+    double* d_c = h_c ? reinterpret_cast<double*>(h->io + ccofs) : nullptr;
+    IDK_CUDA(cudaMemcpyAsync(d_a, h_a, sizeof(double) * m * n, cudaMemcpyHostToDevice, h->stream));
+    rc = id_auto_dev(h, d_a, m, n, m, k, method, seed, p, omega_mode, nullptr, d_cols, d_z, d_c, transposed);
+    if (rc) return rc;
+    IDK_CUDA(cudaMemcpyAsync(h_cols, d_cols, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaMemcpyAsync(h_z, d_z, sizeof(double) * k * zc, cudaMemcpyDeviceToHost, h->stream));
+    if (h_c) IDK_CUDA(cudaMemcpyAsync(h_c, d_c, sizeof(double) * crow * k, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    return IDK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (internal to the C-ABI library).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace idk {
+
+// sketch_gemm.cu
+int sketch_gemm_pick_wm(int M);
+int sketch_gemm_pick_splits(int M, int64_t N, int64_t K, int num_sms);
+cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans, double* Y,
+                        int64_t ldc, int M, int64_t N, int64_t K, int splits, double* partial, cudaStream_t stream);
+cudaError_t omega_philox(double* out, int64_t l, int64_t m, uint64_t seed, cudaStream_t stream);
+
+// cpqr.cu
+constexpr size_t kCpqrPubBytes = 32;
+size_t cpqr_smem_bytes(int m, int cols_per_cta);
+cudaError_t cpqr_launch(double* W, int64_t ldw, int m, int64_t n, int k, long long* pos_out, long long* pivots,
+                        double* taus, void* ws_pub, unsigned* barrier, int num_sms, int max_ctas,
+                        cudaStream_t stream);
+cudaError_t cpqr_finish(const double* W, int64_t ldw, int m, int64_t n, int k, const long long* pos,
+                        const long long* pivots, const double* taus, long long* perm, double* R, double* Q,
+                        cudaStream_t stream);
+
+// trsm.cu
+int id_trsm_nb(int k);
+size_t id_trsm_smem_bytes(int k);
+cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t n, const long long* pivots, const long long* pos,
+                       double* R11, int* status, double* Z, cudaStream_t stream);
+cudaError_t gather_columns(const double* A, int64_t lda, int64_t rows, const long long* cols, int k, bool rows_of_a,
+                           double* C, cudaStream_t stream);
+cudaError_t copy_pivots(const long long* src, int k, long long* dst, cudaStream_t stream);
+
+// batched.cu
+size_t batched_id_smem_bytes(int m, int n);
+cudaError_t batched_id(const double* A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
+                       long long* cols, double* Z, double* C, int* status, cudaStream_t stream);
+
+// util.cu
+cudaError_t transpose_copy(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb,
+                           cudaStream_t stream);
+
+}  // namespace idk

@@ -1,0 +1,319 @@
+// sketch_gemm.cu -- Y = Omega * A (or Omega * A^T) in fp64 on the DMMA tensor pipe.
+//
+// Replaces the reference's Y = matmul(Omega, A) of the composed sketch oracle
+// (matrix.cpp:28-48 called on generate(gaussian, l, m, seed), datasets.cpp:15-33).
+// Omega is l x K column-major (l = k + p is small: 72..272), A is the big
+// matrix.  Two B layouts:
+//   * kNT = false : B[kk, j] = A[kk + j*ldb]   (A is K x n, column-major)
+//   * kNT = true  : B[kk, j] = A[j + kk*ldb]   (A is n x K, column-major; the
+//                   id_auto dual Y = Omega * A^T without materialising A^T,
+//                   id.cpp:85)
+// CTA tile BM x 64 x 16 (BM = 16*WM, chosen so BM covers l with little
+// padding), 4 warps in 2 x 2, warp tile (8*WM) x 32 of m8n8k4 DMMA tiles,
+// 3-stage cp.async pipeline, optional split-K with a fixed-order reduction so
+// results are bit-reproducible run to run.
+#include "common.cuh"
+
+namespace idk {
+
+namespace {
+
+constexpr int kBN = 64;
+constexpr int kBK = 16;
+constexpr int kStages = 3;
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int WM, bool kNT>
+struct Smem {
+    static constexpr int BM = 16 * WM;
+    static constexpr int SA = BM + 4;                  // As[kk][i], stride = 4 mod 16 doubles
+    static constexpr int SB = kNT ? (kBN + 4) : (kBK + 4);  // Bs[kk][j] or Bs[j][kk]
+    static constexpr int A_ELEMS = kBK * SA;
+    static constexpr int B_ELEMS = kNT ? kBK * SB : kBN * SB;
+    static constexpr int STAGE = A_ELEMS + B_ELEMS;
+    static constexpr size_t BYTES = sizeof(double) * STAGE * kStages;
+};
+
+template <int WM, bool kNT>
+__global__ void __launch_bounds__(kThreads)
+sketch_gemm_kernel(const double* __restrict__ A, int64_t lda,  // Omega: l x K
+                   const double* __restrict__ B, int64_t ldb,  // big matrix
+                   double* __restrict__ C, int64_t ldc,        // Y (or split-K partial base)
+                   int64_t split_stride,                       // elements between split partials
+                   int M, int64_t N, int64_t K, int64_t k_per_split, bool vec16) {
+    using S = Smem<WM, kNT>;
+    constexpr int BM = S::BM;
+    extern __shared__ __align__(16) double smem[];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int m0 = blockIdx.x * BM;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.y) * kBN;
+    const int64_t kbeg = static_cast<int64_t>(blockIdx.z) * k_per_split;
+    const int64_t kend = min(K, kbeg + k_per_split);
+    const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBK - 1) / kBK) : 0;
+    C += static_cast<int64_t>(blockIdx.z) * split_stride;
+
+    auto load_stage = [&](int stage, int kt) {
+        double* As = smem + stage * S::STAGE;
+        double* Bs = As + S::A_ELEMS;
+        const int64_t k0 = kbeg + static_cast<int64_t>(kt) * kBK;
+        // A tile: kBK columns of Omega, BM contiguous rows each.
+        if (vec16) {
+            for (int e = tid; e < kBK * (BM / 2); e += kThreads) {
+                const int kk = e / (BM / 2), i = (e % (BM / 2)) * 2;
+                const int64_t gk = k0 + kk;
+                const int gi = m0 + i;
+                int bytes = 0;
+                if (gk < kend && gi < M) bytes = (gi + 1 < M) ? 16 : 8;
+                const double* src = bytes ? A + gk * lda + gi : A;
+                cp_async_16(As + kk * S::SA + i, src, bytes);
+            }
+        } else {
+            for (int e = tid; e < kBK * BM; e += kThreads) {
+                const int kk = e / BM, i = e % BM;
+                const int64_t gk = k0 + kk;
+                const int gi = m0 + i;
+                const bool ok = gk < kend && gi < M;
+                cp_async_8(As + kk * S::SA + i, ok ? A + gk * lda + gi : A, ok);
+            }
+        }
+        if constexpr (!kNT) {
+            // B tile: kBN columns of A, kBK contiguous k each -> Bs[j][kk].
+            if (vec16) {
+                for (int e = tid; e < kBN * (kBK / 2); e += kThreads) {
+                    const int j = e / (kBK / 2), kk = (e % (kBK / 2)) * 2;
+                    const int64_t gj = n0 + j, gk = k0 + kk;
+                    int bytes = 0;
+                    if (gj < N && gk < kend) bytes = (gk + 1 < kend) ? 16 : 8;
+                    const double* src = bytes ? B + gj * ldb + gk : B;
+                    cp_async_16(Bs + j * S::SB + kk, src, bytes);
+                }
+            } else {
+                for (int e = tid; e < kBN * kBK; e += kThreads) {
+                    const int j = e / kBK, kk = e % kBK;
+                    const int64_t gj = n0 + j, gk = k0 + kk;
+                    const bool ok = gj < N && gk < kend;
+                    cp_async_8(Bs + j * S::SB + kk, ok ? B + gj * ldb + gk : B, ok);
+                }
+            }
+        } else {
+            // B tile: kBK rows of A^T = kBK columns of A (n x K), kBN contiguous j each -> Bs[kk][j].
+            if (vec16) {
+                for (int e = tid; e < kBK * (kBN / 2); e += kThreads) {
+                    const int kk = e / (kBN / 2), j = (e % (kBN / 2)) * 2;
+                    const int64_t gj = n0 + j, gk = k0 + kk;
+                    int bytes = 0;
+                    if (gk < kend && gj < N) bytes = (gj + 1 < N) ? 16 : 8;
+                    const double* src = bytes ? B + gk * ldb + gj : B;
+                    cp_async_16(Bs + kk * S::SB + j, src, bytes);
+                }
+            } else {
+                for (int e = tid; e < kBK * kBN; e += kThreads) {
+                    const int kk = e / kBN, j = e % kBN;
+                    const int64_t gj = n0 + j, gk = k0 + kk;
+                    const bool ok = gk < kend && gj < N;
+                    cp_async_8(Bs + kk * S::SB + j, ok ? B + gk * ldb + gj : B, ok);
+                }
+            }
+        }
+    };
+
+    double acc[WM][4][2];
+#pragma unroll
+    for (int a = 0; a < WM; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < ktiles) load_stage(s, s);
+        cp_async_commit();
+    }
+
+    const int fr = lane >> 2, fc = lane & 3;
+    for (int kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        {
+            const int nk = kt + kStages - 1;
+            if (nk < ktiles) load_stage(nk % kStages, nk);
+            cp_async_commit();
+        }
+        const double* As = smem + (kt % kStages) * S::STAGE;
+        const double* Bs = As + S::A_ELEMS;
+#pragma unroll
+        for (int kq = 0; kq < kBK / 4; ++kq) {
+            double af[WM], bf[4];
+#pragma unroll
+            for (int tm = 0; tm < WM; ++tm) af[tm] = As[(kq * 4 + fc) * S::SA + wm * (8 * WM) + tm * 8 + fr];
+#pragma unroll
+            for (int tn = 0; tn < 4; ++tn) {
+                const int j = wn * 32 + tn * 8 + fr;
+                if constexpr (kNT)
+                    bf[tn] = Bs[(kq * 4 + fc) * S::SB + j];
+                else
+                    bf[tn] = Bs[j * S::SB + kq * 4 + fc];
+            }
+#pragma unroll
+            for (int tm = 0; tm < WM; ++tm)
+#pragma unroll
+                for (int tn = 0; tn < 4; ++tn) dmma_8x8x4(acc[tm][tn], af[tm], bf[tn]);
+        }
+    }
+    cp_async_wait<0>();
+
+#pragma unroll
+    for (int tm = 0; tm < WM; ++tm) {
+        const int i = m0 + wm * (8 * WM) + tm * 8 + fr;
+        if (i >= M) continue;
+#pragma unroll
+        for (int tn = 0; tn < 4; ++tn) {
+            const int64_t j = n0 + wn * 32 + tn * 8 + 2 * fc;
+            if (j < N) C[j * ldc + i] = acc[tm][tn][0];
+            if (j + 1 < N) C[(j + 1) * ldc + i] = acc[tm][tn][1];
+        }
+    }
+}
+
+// Fixed-order split-K reduction: Y = sum_{s=0}^{S-1} P_s (s ascending).
+__global__ void splitk_reduce_kernel(const double* __restrict__ P, int64_t split_stride, int splits,
+                                     double* __restrict__ Y, int M, int64_t N, int64_t ldc) {
+    const int64_t total = static_cast<int64_t>(M) * N;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / M;
+        const int i = static_cast<int>(e - j * M);
+        const int64_t off = j * ldc + i;
+        double s = P[off];
+        for (int t = 1; t < splits; ++t) s += P[t * split_stride + off];
+        Y[off] = s;
+    }
+}
+
+template <int WM, bool kNT>
+cudaError_t launch_wm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                      int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K, int splits,
+                      bool vec16, cudaStream_t stream) {
+    using S = Smem<WM, kNT>;
+    auto kern = sketch_gemm_kernel<WM, kNT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(S::BYTES));
+    if (e != cudaSuccess) return e;
+    int64_t kps = (K + splits - 1) / splits;
+    kps = ((kps + kBK - 1) / kBK) * kBK;
+    dim3 grid((M + S::BM - 1) / S::BM, static_cast<unsigned>((N + kBN - 1) / kBN), splits);
+    kern<<<grid, kThreads, S::BYTES, stream>>>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, kps,
+                                               vec16);
+    return cudaGetLastError();
+}
+
+template <bool kNT>
+cudaError_t launch_nt(int wm, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                      int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K, int splits,
+                      bool vec16, cudaStream_t stream) {
+    switch (wm) {
+        case 2: return launch_wm<2, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
+        case 3: return launch_wm<3, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
+        case 4: return launch_wm<4, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
+        case 5: return launch_wm<5, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
+        case 6: return launch_wm<6, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
+        default: return launch_wm<7, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
+    }
+}
+
+}  // namespace
+
+// Pick BM = 16*WM (WM in 2..7) minimising padded rows over ceil(M/BM) tiles.
+int sketch_gemm_pick_wm(int M) {
+    int best = 7;
+    int64_t best_pad = INT64_MAX;
+    for (int wm = 7; wm >= 2; --wm) {
+        const int bm = 16 * wm;
+        const int64_t tiles = (M + bm - 1) / bm;
+        const int64_t pad = tiles * bm - M + tiles * 4;  // small bias toward fewer tiles
+        if (pad < best_pad) {
+            best_pad = pad;
+            best = wm;
+        }
+    }
+    return best;
+}
+
+// Number of K splits so the grid covers the SMs ~4x.
+int sketch_gemm_pick_splits(int M, int64_t N, int64_t K, int num_sms) {
+    const int wm = sketch_gemm_pick_wm(M);
+    const int64_t tiles = ((M + 16 * wm - 1) / (16 * wm)) * ((N + kBN - 1) / kBN);
+    int splits = 1;
+    while (tiles * splits < 3LL * num_sms && K / (splits * 2) >= 256 && splits < 16) splits *= 2;
+    return splits;
+}
+
+// Y (M x N, ldc) = A (M x K, lda) * op(B); op(B) = B (K x N, ldb) or B^T (B is N x K, ldb).
+// `partial` must hold splits * ldc * N doubles when splits > 1.
+cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans,
+                        double* Y, int64_t ldc, int M, int64_t N, int64_t K, int splits,
+                        double* partial, cudaStream_t stream) {
+    if (M <= 0 || N <= 0) return cudaSuccess;
+    const int wm = sketch_gemm_pick_wm(M);
+    const bool vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+    if (splits < 1) splits = 1;
+    double* out = splits > 1 ? partial : Y;
+    const int64_t split_stride = ldc * N;
+    cudaError_t e = b_trans ? launch_nt<true>(wm, A, lda, B, ldb, out, ldc, split_stride, M, N, K, splits, vec16, stream)
+                            : launch_nt<false>(wm, A, lda, B, ldb, out, ldc, split_stride, M, N, K, splits, vec16, stream);
+    if (e != cudaSuccess || splits == 1) return e;
+    const int64_t total = static_cast<int64_t>(M) * N;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(partial, split_stride, splits, Y, M, N, ldc);
+    return cudaGetLastError();
+}
+
+// Omega (l x m, column-major, ld = l) from Philox4x32-10 keyed by seed.
+}  // namespace idk
+
+#include "rng.cuh"
+
+namespace idk {
+namespace {
+__global__ void omega_philox_kernel(double* __restrict__ out, int64_t total, uint64_t seed) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[e] = philox_normal(static_cast<uint64_t>(e), seed);
+}
+}  // namespace
+
+cudaError_t omega_philox(double* out, int64_t l, int64_t m, uint64_t seed, cudaStream_t stream) {
+    const int64_t total = l * m;
+    if (total <= 0) return cudaSuccess;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    omega_philox_kernel<<<blocks, 256, 0, stream>>>(out, total, seed);
+    return cudaGetLastError();
+}
+
+}  // namespace idk

@@ -1,0 +1,302 @@
+"""Host-side mirror of the reference's ID interface (proj/include/idkit/id.hpp,
+qr.hpp, matrix.hpp) over the B200 C ABI.
+
+Same names, argument meaning and error behaviour as the reference:
+
+  reference (C++)                                 here
+  ----------------------------------------------  ---------------------------------------------
+  IdResult optim_id(const Matrix&, k)   id.hpp:40  optim_id(a, k)
+  (sketch RID composed from the reference API)   sketch_rid(a, k, p, seed, omega_mode, omega)
+  IdResult id_auto(a, k, method, seed, frac)      id_auto(a, k, method, seed, p=...)
+  PivotedQr qr_column_pivoted(a, steps) qr.hpp:34 qr_column_pivoted(a, steps)
+  Matrix select_columns(a, cols)    matrix.hpp:76 select_columns(a, cols)
+  std::invalid_argument                           InvalidArgument (a ValueError)
+  SingularMatrixError / NotPositiveDefiniteError  same names
+
+Matrices are torch CUDA fp64 tensors in column-major layout (shape (m, n),
+strides (1, lda)) -- the idkit::Matrix storage contract -- or numpy arrays,
+which are routed through the host-buffer entry (copies inside the call).
+Results come back on the same side they went in.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+
+OMEGA_PHILOX, OMEGA_MT19937, OMEGA_VERBATIM = 0, 1, 2
+DETERMINISTIC, RANDOMIZED = 0, 1
+
+
+class IdkitError(RuntimeError):
+    pass
+
+
+class InvalidArgument(IdkitError, ValueError):
+    """std::invalid_argument in the reference (id.cpp:14-18, qr.cpp:45-46)."""
+
+
+class SingularMatrixError(IdkitError):
+    """idkit::SingularMatrixError (errors.hpp:9-13)."""
+
+
+class NotPositiveDefiniteError(IdkitError):
+    """idkit::NotPositiveDefiniteError (errors.hpp:15-19)."""
+
+
+class CudaError(IdkitError):
+    pass
+
+
+_ERRORS = {1: InvalidArgument, 2: SingularMatrixError, 3: NotPositiveDefiniteError, 4: CudaError,
+           5: CudaError, 6: CudaError}
+
+
+@dataclass
+class IdResult:
+    """id.hpp:17-22.  `approx` is not materialised (next row);
+    `c` is C = A[:, cols] (rows of A when transposed)."""
+    cols: object
+    z: object
+    c: Optional[object] = None
+    transposed: bool = False
+
+
+@dataclass
+class PivotedQr:
+    """qr.hpp:16-21."""
+    q: object
+    r: object
+    perm: object
+    steps: int
+
+
+class Context:
+    """One idk_handle bound to a device; one per thread (handles are not shared)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        rc = self.lib.idk_create(C.byref(h), device)
+        if rc != 0:
+            raise CudaError(f"idk_create(device={device}) failed: {self.lib.idk_status_string(rc).decode()} "
+                            "(no usable sm_100 GPU; there is no CPU fallback)")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.idk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int):
+        if rc != 0:
+            msg = self.lib.idk_last_error(self.h).decode()
+            raise _ERRORS.get(rc, IdkitError)(msg)
+
+    def bind_stream(self):
+        import torch
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        self.lib.idk_set_stream(self.h, C.c_void_p(s))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.idk_kernel_launches(self.h))
+
+
+_tls = threading.local()
+
+
+def context(device: int = 0) -> Context:
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+# ---- layout helpers -----------------------------------------------------------
+
+def is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def fortran(t):
+    """Column-major view/copy of a 2-D fp64 CUDA tensor: strides (1, ld)."""
+    import torch
+    if t.dtype != torch.float64:
+        raise InvalidArgument("matrices are fp64 (idkit::Matrix stores double)")
+    if t.dim() != 2:
+        raise InvalidArgument("expected a 2-D matrix")
+    if t.stride(0) == 1 and t.stride(1) >= max(1, t.shape[0]):
+        return t
+    return t.t().contiguous().t()
+
+
+def empty_f(m: int, n: int, device):
+    import torch
+    return torch.empty((n, m), dtype=torch.float64, device=device).t()
+
+
+def _ld(t) -> int:
+    return max(int(t.stride(1)), 1)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+# ---- the ID path ----------------------------------------------------------------
+
+def optim_id(a, k: int, want_c: bool = True) -> IdResult:
+    """Deterministic ID (id.hpp:40).  Z in the interpolation form [I | R11^-1 R12] P^T."""
+    import torch
+    if not is_torch(a):
+        r = optim_id(torch.from_numpy(np.asfortranarray(a, dtype=np.float64)).cuda(), k, want_c)
+        return IdResult(r.cols.cpu().numpy(), r.z.cpu().numpy(), None if r.c is None else r.c.cpu().numpy(), False)
+    a = fortran(a)
+    m, n = a.shape
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    cols = torch.empty(max(k, 0), dtype=torch.int64, device=a.device)
+    z = empty_f(max(k, 0), n, a.device)
+    c = empty_f(m, max(k, 0), a.device) if want_c else None
+    ctx.check(ctx.lib.idk_optim_id(ctx.h, _ptr(a), m, n, _ld(a), k, _ptr(cols), _ptr(z), _ptr(c)))
+    return IdResult(cols, z, c, False)
+
+
+def sketch_rid(a, k: int, p: int, seed: int = 0, omega_mode: int = OMEGA_PHILOX, omega=None,
+               transposed: bool = False, want_c: bool = True) -> IdResult:
+    """Gaussian-sketch RID.  `a` is M (m x n) or, with transposed=True, the stored
+    n x m matrix whose transpose is decomposed (id_auto dual without A^T)."""
+    import torch
+    a = fortran(a)
+    if transposed:
+        n, m = a.shape
+    else:
+        m, n = a.shape
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    om = fortran(omega) if omega is not None else None
+    if omega_mode == OMEGA_VERBATIM and (om is None or om.shape != (k + p, m) or _ld(om) != k + p):
+        raise InvalidArgument("verbatim omega must be a packed (k+p) x m fp64 CUDA matrix")
+    cols = torch.empty(max(k, 0), dtype=torch.int64, device=a.device)
+    z = empty_f(max(k, 0), n, a.device)
+    c = empty_f(m, max(k, 0), a.device) if want_c else None
+    ctx.check(ctx.lib.idk_sketch_rid(ctx.h, _ptr(a), m, n, _ld(a), 1 if transposed else 0, k, p, seed,
+                                     omega_mode, _ptr(om), _ptr(cols), _ptr(z), _ptr(c)))
+    return IdResult(cols, z, c, transposed)
+
+
+def id_auto(a, k: int, method: int = DETERMINISTIC, seed: int = 0, p: int = 0,
+            omega_mode: int = OMEGA_PHILOX, want_c: bool = True) -> IdResult:
+    """id.hpp:55-56: tall inputs (m > n) are decomposed through their transpose.
+    `p` is the sketch oversampling (rows of Omega = k + p) for method=RANDOMIZED."""
+    m, n = a.shape
+    tall = m > n
+    zc = m if tall else n
+    crow = n if tall else m
+    if is_torch(a):
+        import torch
+        a = fortran(a)
+        ctx = context(a.device.index or 0)
+        ctx.bind_stream()
+        cols = torch.empty(max(k, 0), dtype=torch.int64, device=a.device)
+        z = empty_f(max(k, 0), zc, a.device)
+        c = empty_f(crow, max(k, 0), a.device) if want_c else None
+        tr = C.c_int(0)
+        ctx.check(ctx.lib.idk_id_auto(ctx.h, _ptr(a), m, n, _ld(a), k, method, seed, p, omega_mode, None,
+                                      _ptr(cols), _ptr(z), _ptr(c), C.byref(tr)))
+        return IdResult(cols, z, c, bool(tr.value))
+    a = np.asfortranarray(a, dtype=np.float64)
+    ctx = context(0)
+    cols = np.empty(max(k, 0), dtype=np.int64)
+    z = np.empty((max(k, 0), zc), order="F")
+    c = np.empty((crow, max(k, 0)), order="F") if want_c else None
+    tr = C.c_int(0)
+    ctx.check(ctx.lib.idk_id_auto_host(ctx.h, a.ctypes.data_as(C.c_void_p), m, n, k, method, seed, p, omega_mode,
+                                       cols.ctypes.data_as(C.c_void_p), z.ctypes.data_as(C.c_void_p),
+                                       c.ctypes.data_as(C.c_void_p) if c is not None else None, C.byref(tr)))
+    return IdResult(cols, z, c, bool(tr.value))
+
+
+def optim_id_batched(a, k: int, want_c: bool = True):
+    """BASELINE cfg3: `a` is a (batch, n, m) contiguous CUDA tensor holding
+    batch column-major m x n matrices (i.e. a[b].t() is matrix b).
+    Returns cols (batch, k), z (batch, n, k) [= Z_b^T row-major], c (batch, k, m)."""
+    import torch
+    if a.dim() != 3 or not a.is_contiguous() or a.dtype != torch.float64:
+        raise InvalidArgument("batched input must be a contiguous (batch, n, m) fp64 tensor")
+    batch, n, m = a.shape
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    cols = torch.empty((batch, max(k, 0)), dtype=torch.int64, device=a.device)
+    z = torch.empty((batch, n, max(k, 0)), dtype=torch.float64, device=a.device)
+    c = torch.empty((batch, max(k, 0), m), dtype=torch.float64, device=a.device) if want_c else None
+    ctx.check(ctx.lib.idk_optim_id_batched(ctx.h, _ptr(a), batch, m, n, m, m * n, k, _ptr(cols), _ptr(z),
+                                           _ptr(c)))
+    return cols, z, c
+
+
+# ---- stages / primitives ----------------------------------------------------------
+
+def sketch_omega(l: int, m: int, seed: int, device=0):
+    import torch
+    ctx = context(device)
+    ctx.bind_stream()
+    om = empty_f(l, m, torch.device("cuda", device))
+    ctx.check(ctx.lib.idk_sketch_omega(ctx.h, l, m, seed, _ptr(om)))
+    return om
+
+
+def sketch(omega, a, transposed: bool = False):
+    """Y = Omega * M (matrix.cpp:28-48 on the DMMA pipe)."""
+    omega = fortran(omega)
+    a = fortran(a)
+    l, m = omega.shape
+    n = a.shape[0] if transposed else a.shape[1]
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    y = empty_f(l, n, a.device)
+    ctx.check(ctx.lib.idk_sketch(ctx.h, _ptr(omega), l, _ptr(a), m, n, _ld(a), 1 if transposed else 0, _ptr(y), l))
+    return y
+
+
+def qr_column_pivoted(a, steps: int, want_q: bool = True) -> PivotedQr:
+    """qr.hpp:34."""
+    import torch
+    a = fortran(a)
+    m, n = a.shape
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    q = empty_f(m, max(steps, 0), a.device) if want_q else None
+    r = empty_f(max(steps, 0), n, a.device)
+    perm = torch.empty(n, dtype=torch.int64, device=a.device)
+    ctx.check(ctx.lib.idk_qr_column_pivoted(ctx.h, _ptr(a), m, n, _ld(a), steps, _ptr(q), _ptr(r), _ptr(perm)))
+    return PivotedQr(q, r, perm, steps)
+
+
+def select_columns(a, cols, rows_of_a: bool = False):
+    """matrix.hpp:76 (rows_of_a: the dual's row gather)."""
+    import torch
+    a = fortran(a)
+    m, n = a.shape
+    cols = torch.as_tensor(cols, dtype=torch.int64, device=a.device).contiguous()
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    out = empty_f(n if rows_of_a else m, cols.numel(), a.device)
+    ctx.check(ctx.lib.idk_select_columns(ctx.h, _ptr(a), m, n, _ld(a), _ptr(cols), cols.numel(),
+                                         1 if rows_of_a else 0, _ptr(out)))
+    return out
