@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200 ID path on BASELINE.json's workload.
+
+Default workload (N=1): BASELINE configs[1] ("cfg2"): Gaussian-sketch RID of a
+2000 x 4000 fp64 A = U diag(exp(-i/30)) V^T, k = 100, p = 10, Omega from the
+on-device Philox generator.  A "step" is one full ID (sketch -> CPQR -> Z ->
+C) through the C ABI (idk_sketch_rid), inputs already resident in HBM.  L2
+(126 MB) is flushed with a 256 MiB memset between timed steps (A is 64 MB);
+only the step itself is inside the CUDA events.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1..cfg5]
+  python bench.py --impl reference ...   # the reference's CPU path (oracle/_ref)
+
+N > 1 is launched by torchrun, one rank per GPU; cfg1/cfg2 run as independent
+replicas ("replicas only"), cfg3 partitions the batch by matrix.
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "IDs/sec & achieved HBM GB/s / FP64 TFLOPS at 1/2/4/8 B200 vs CPU ref"
+UNIT = "IDs/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--seed", type=int, default=20260601)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def workload_desc(cfg):
+    if cfg.name == "cfg3":
+        return f"{cfg.name}: batched deterministic ID, {cfg.batch} x {cfg.m}x{cfg.n} fp64, k={cfg.k}"
+    if cfg.randomized:
+        return (f"{cfg.name}: Gaussian-sketch RID {cfg.m}x{cfg.n} fp64, k={cfg.k}, p={cfg.p}, "
+                f"Omega on device (Philox)" + (" , id_auto dual (m > n)" if cfg.m > cfg.n else ""))
+    return f"{cfg.name}: deterministic ID {cfg.m}x{cfg.n} fp64, k={cfg.k}"
+
+
+def ids_per_step(cfg):
+    return cfg.batch if cfg.name == "cfg3" else 1
+
+
+# ---------------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s >= 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------
+def stage_work(cfg, n_local):
+    """Algorithmic bytes / flops per launch of each stage; DESIGN.md states them."""
+    m, n, k = cfg.m, n_local, cfg.k
+    if cfg.m > cfg.n:  # dual: the ID runs on A^T (n x m)
+        m, n = cfg.n, cfg.m
+    l = cfg.l if cfg.randomized else m
+    return {
+        "sketch": {"flops": 2.0 * l * m * n, "bytes": 8.0 * (m * n + l * m + l * n)},
+        "cpqr": {"bytes": 8.0 * 2 * l * n, "flops": sum(4.0 * (l - s) * (n - s - 1) for s in range(k))},
+        "solve": {"bytes": 8.0 * 2 * k * n, "flops": float(k) * k * (n - k)},
+        "gather": {"bytes": 8.0 * 2 * m * k},
+        "prep": {"bytes": 8.0 * l * m if cfg.randomized else 8.0 * 2 * m * n},
+    }
+
+
+def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic):
+    secs = avg_ms / 1e3
+    if stage == "sketch":
+        achieved = work["flops"] / secs / 1e12
+        return {"kernel": "sketch_gemm_kernel (DMMA m8n8k4)", "bound": "tensor", "achieved": achieved,
+                "peak": fp64_peak["tflops"], "unit": "TFLOP/s", "frac": achieved / fp64_peak["tflops"],
+                "peak_source": fp64_peak["source"], "traffic": traffic, "avg_launch_ms": avg_ms,
+                "algorithmic_per_launch": work["flops"]}
+    achieved = work["bytes"] / secs / 1e9
+    names = {"cpqr": "cpqr_persistent_kernel", "solve": "gather_r11_kernel + id_trsm_kernel",
+             "gather": "gather_columns_kernel", "prep": "omega_philox_kernel / working copy",
+             "batched": "batched_id_kernel"}
+    return {"kernel": names.get(stage, stage), "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)", "traffic": traffic, "avg_launch_ms": avg_ms,
+            "algorithmic_per_launch": work["bytes"]}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2105_07076_b200 as idk
+    from paper_2105_07076_b200.configs import CONFIGS, make_torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+
+    # ---- inputs (harness; not timed) ----
+    seed = args.seed + (rank if cfg.name in ("cfg1", "cfg2") else 0)
+    a = make_torch(cfg.name, seed=seed, device=f"cuda:{local}")
+    if cfg.name == "cfg3" and world > 1:  # partition by matrix, no collective
+        per = (cfg.batch + world - 1) // world
+        a = a[rank * per:min(cfg.batch, (rank + 1) * per)].contiguous()
+    ctx = idk.context(local)
+    ctx.set_profiling(True)
+    k, p = cfg.k, max(cfg.p, 0)
+
+    def step():
+        if cfg.name == "cfg3":
+            return idk.optim_id_batched(a, k)
+        if cfg.randomized:
+            return idk.id_auto(a, k, idk.RANDOMIZED, seed=args.seed, p=p)
+        return idk.id_auto(a, k, idk.DETERMINISTIC)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.1)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stage_tot = {}
+    launches0 = ctx.kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    for i in range(args.steps):
+        flush.zero_()
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+        if cfg.name != "cfg3":
+            for kname, v in ctx.stage_times().items():
+                stage_tot[kname] = stage_tot.get(kname, 0.0) + v
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = ctx.kernel_launches - launches0
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    clocks = sampler.stop()
+
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    total_ids = ids_per_step(cfg) * args.steps * (world if cfg.name != "cfg3" else 1)
+    if cfg.name == "cfg3" and world > 1:
+        total_ids = cfg.batch * args.steps
+    value = total_ids / (max_ms / 1e3)
+
+    # ---- e2e through the public host-buffer API (H2D + compute + D2H each step) ----
+    e2e = None
+    if not args.no_e2e and cfg.name != "cfg3":
+        pinned = torch.empty((cfg.n, cfg.m), dtype=torch.float64).pin_memory()
+        pinned.copy_(a.t().cpu())
+        ha = pinned.numpy().T  # F-ordered view of pinned memory
+        assert ha.flags["F_CONTIGUOUS"]
+        ke = max(1, min(args.steps, 20))
+        for _ in range(2):
+            idk.id_auto(ha, k, idk.RANDOMIZED if cfg.randomized else idk.DETERMINISTIC, seed=args.seed, p=p)
+        torch.cuda.synchronize(dev)
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+        if world > 1:
+            dist.barrier()
+        for i in range(ke):
+            flush.zero_()
+            ev0[i].record(stream)
+            r = idk.id_auto(ha, k, idk.RANDOMIZED if cfg.randomized else idk.DETERMINISTIC, seed=args.seed, p=p)
+            ev1[i].record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = torch.tensor([sum(x.elapsed_time(y) for x, y in zip(ev0, ev1))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        zc = max(cfg.m, cfg.n)
+        crow = min(cfg.m, cfg.n) if cfg.m > cfg.n else cfg.m
+        e2e = {"value": world * ke / (float(e_ms.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * cfg.m * cfg.n,
+               "d2h_bytes_per_step": 8 * k + 8 * k * zc + 8 * crow * k,
+               "api": "idk_id_auto_host (include/idkit_b200.h), pinned host buffers"}
+        del r
+
+    # ---- roofline of the dominant kernel ----
+    peaks = load_json(PEAKS_FILE) or {"hbm_gbs": 6650.0, "_fallback": True}
+    fp64 = load_json(FP64_PEAK_FILE) or {"tflops": 37.15, "source": "fallback: tools/probe_fp64.cu DMMA loop"}
+    fp64.setdefault("source", "tools/probe_fp64.cu")
+    ncu = load_json(NCU_SUMMARY) or {}
+    roofline = None
+    stage_avg = {}
+    if cfg.name != "cfg3" and stage_tot:
+        stage_avg = {s: v / args.steps for s, v in stage_tot.items()}
+        dom = max(stage_avg, key=stage_avg.get)
+        traffic = (ncu.get(cfg.name) or {}).get(dom, {}).get("dram_bytes_per_launch")
+        roofline = roofline_for(dom, stage_work(cfg, cfg.n)[dom], stage_avg[dom], peaks, fp64, traffic)
+        roofline["step_share"] = stage_avg[dom] / (max_ms / args.steps)
+    elif cfg.name == "cfg3":
+        per = a.shape[0]
+        bytes_ = 8.0 * per * (cfg.m * cfg.n + cfg.k * cfg.n + cfg.m * cfg.k) + 8.0 * per * cfg.k
+        traffic = (ncu.get(cfg.name) or {}).get("batched", {}).get("dram_bytes_per_launch")
+        roofline = roofline_for("batched", {"bytes": bytes_}, total_ms / args.steps, peaks, fp64, traffic)
+    if peaks.get("_fallback") and roofline:
+        roofline["peak_source"] = "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+    # ---- cpu baseline (rank 0, N=1, bounded sample) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, a, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded BASELINE construction (" + cfg.name + "), generated on device",
+            "config": {"workload": workload_desc(cfg), "m": cfg.m, "n": cfg.n, "k": cfg.k, "p": cfg.p,
+                       "batch": cfg.batch,
+                       "parallelism": ("replicas" if cfg.name in ("cfg1", "cfg2") else "partition-by-matrix")
+                       + f" x{world}",
+                       "l2": "flushed between timed steps (256 MiB memset, outside the events)",
+                       "inputs": "resident in HBM"},
+            "stages_ms_per_step": stage_avg or None,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------
+# reference CPU path (oracle/_ref = the reference sources compiled in place)
+# ---------------------------------------------------------------------------------
+def _ref_lib():
+    from oracle import Oracle, Reference
+    if Reference.available():
+        return Reference(), "reference"
+    return Oracle(), "port"
+
+
+def _ref_call(lib, kind, cfg, a, omega):
+    if cfg.name == "cfg3":
+        for b in range(a.shape[0]):
+            ab = a[b].T
+            if kind == "reference":
+                lib.sketch_id(ab, cfg.k, None, want_c=True)
+            else:
+                lib.interp_decomp(ab, cfg.k)
+        return
+    if kind == "reference":
+        lib.sketch_id(a, cfg.k, omega, want_c=True)
+    else:
+        lib.interp_decomp(a, cfg.k, omega)
+
+
+def _ref_inputs(cfg, a_dev=None, seed=20260601, cfg3_sample=64):
+    import numpy as np
+    from oracle import Oracle
+    from paper_2105_07076_b200.configs import make_np
+    if cfg.name == "cfg3":
+        a = make_np("cfg3", seed=seed, scale=cfg3_sample / cfg.batch)
+        return a, None
+    if a_dev is not None:
+        a = a_dev.cpu().numpy()
+        a = np.asfortranarray(a)
+    else:
+        a = make_np(cfg.name, seed=seed)
+    if cfg.m > cfg.n:
+        a = np.asfortranarray(a.T)  # the dual runs on A^T (id.cpp:85)
+    omega = Oracle().omega_philox(cfg.l, a.shape[0], seed) if cfg.randomized else None
+    return a, omega
+
+
+def _timed_parallel(lib, kind, cfg, a, omega, threads):
+    errs = []
+
+    def work():
+        try:
+            _ref_call(lib, kind, cfg, a, omega)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work) for _ in range(threads)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    dt = time.perf_counter() - t0
+    if errs:
+        raise errs[0]
+    return dt
+
+
+def cpu_baseline(cfg, a_dev, args):
+    """The reference's CPU path on this host: bounded sample, 1 thread (the reference is single-threaded)."""
+    if cfg.name in ("cfg4", "cfg5"):
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": "skipped: one reference ID takes minutes at this size (BASELINE.md preview: cfg4 95 s)"}
+    lib, kind = _ref_lib()
+    a, omega = _ref_inputs(cfg, a_dev, seed=args.seed)
+    ids_each = a.shape[0] if cfg.name == "cfg3" else 1
+    dt1 = _timed_parallel(lib, kind, cfg, a, omega, 1)  # warm-up + estimate
+    reps = max(1, int(args.cpu_seconds / max(dt1, 1e-3)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        _ref_call(lib, kind, cfg, a, omega)
+    dt = time.perf_counter() - t0
+    return {"value": reps * ids_each / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{reps} x {'batch of ' + str(ids_each) + ' IDs' if cfg.name == 'cfg3' else 'full ID'} "
+                      f"of {cfg.name} on 1 thread ({dt:.1f} s), composed reference path "
+                      "(matmul -> qr_column_pivoted -> solve_triangular -> select_columns)"}
+
+
+def run_reference(args):
+    from paper_2105_07076_b200.configs import CONFIGS
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    base = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world, "higher_is_better": True,
+            "dtype": "f64", "config": {"workload": workload_desc(cfg), "m": cfg.m, "n": cfg.n, "k": cfg.k,
+                                       "p": cfg.p, "batch": cfg.batch}, "vs_baseline": None}
+    if cfg.name in ("cfg4", "cfg5"):
+        base.update({"unavailable": "one reference ID at this size takes minutes (cfg4 ~95 s on one core)"})
+        print(json.dumps(base), flush=True)
+        return
+    lib, kind = _ref_lib()
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    a, omega = _ref_inputs(cfg, None, seed=args.seed, cfg3_sample=64)
+    ids_each = (a.shape[0] if cfg.name == "cfg3" else 1) * threads
+    t_w = 0.0
+    for _ in range(max(1, min(args.warmup, 1))):
+        t_w = _timed_parallel(lib, kind, cfg, a, omega, threads)
+    budget = 150.0
+    steps = max(1, min(args.steps, int(budget / max(t_w, 1e-3))))
+    total = 0.0
+    for _ in range(steps):
+        total += _timed_parallel(lib, kind, cfg, a, omega, threads)
+    value = steps * ids_each / total
+    sample = (f"each step: {threads} threads x one {cfg.name} ID each" if cfg.name != "cfg3" else
+              f"each step: {threads} threads x 64 of the 4096 {cfg.m}x{cfg.n} matrices") + \
+             f"; {steps} timed steps (requested {args.steps}, capped to ~{budget:.0f} s)"
+    base.update({"value": value, "steps": steps, "warmup": 1, "ms_per_step": 1e3 * total / steps,
+                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(base), flush=True)
+
+
+def main():
+    args = parse()
+    if args.warmup < 3 and args.impl == "ours":
+        print("bench.py: --warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

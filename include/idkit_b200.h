@@ -60,6 +60,13 @@ typedef enum {
     IDK_OMEGA_VERBATIM = 2  /* caller-provided d_omega (l x m, ld = l)                     */
 } idk_omega_mode;
 
+/* Which CPQR kernel factors the pivoted matrix. */
+typedef enum {
+    IDK_CPQR_AUTO = 0,           /* resident, single cluster when it fits, else resident grid, else streaming */
+    IDK_CPQR_RESIDENT_GRID = 1,  /* resident in registers + shared memory, one CTA per SM, grid exchange      */
+    IDK_CPQR_STREAMING = 2       /* trailing matrix streamed through L2 every step (any shape)               */
+} idk_cpqr_mode;
+
 /* ---- handle ---------------------------------------------------------------- */
 IDK_API int idk_abi_version(void);
 IDK_API int idk_create(idk_handle* out, int device);
@@ -70,6 +77,21 @@ IDK_API const char* idk_last_error(idk_handle h);
 IDK_API const char* idk_status_string(int status);
 /* Number of kernels this handle launched since creation (bench evidence). */
 IDK_API int64_t idk_kernel_launches(idk_handle h);
+/* Select the CPQR kernel (idk_cpqr_mode); default IDK_CPQR_AUTO. */
+IDK_API int idk_set_cpqr_mode(idk_handle h, int mode);
+/* The CPQR plan for an m x n, k-step factorisation: out8 = {kind (1 cluster,
+ * 2 resident grid, 3 streaming), CTAs, columns per CTA, threads per column,
+ * register rows per thread, shared-memory rows, threads per CTA, smem bytes}. */
+IDK_API int idk_cpqr_plan(idk_handle h, int64_t m, int64_t n, int64_t k, int64_t* out8);
+/* Debug: record clock64() at 8 phase marks per CPQR step (CTA 0) into d_buf
+ * (k*8 int64, device); NULL turns it off.  Process-wide. */
+IDK_API int idk_debug_cpqr_trace(idk_handle h, int64_t* d_buf);
+/* Record CUDA events at stage boundaries on the handle's stream. */
+IDK_API int idk_set_profiling(idk_handle h, int enable);
+/* Device time (ms) of the last ID call's stages: [0] input prep (Omega or the
+ * working copy of A), [1] sketch GEMM, [2] CPQR, [3] R11 gather + TRSM (Z),
+ * [4] C gather.  Returns the number of entries written (<= 5). */
+IDK_API int idk_stage_times(idk_handle h, double* ms_out, int max_stages);
 
 /* ---- the ID path (device pointers) ----------------------------------------- */
 
@@ -124,8 +146,7 @@ IDK_API int idk_sketch(idk_handle h, const double* d_omega, int64_t l, const dou
                int64_t lda, int a_transposed, double* d_y, int64_t ldy);
 
 /* idkit::qr_column_pivoted (qr.hpp:34, qr.cpp:42-126): q (m x steps, may be
- * NULL), r (steps x n, may be NULL), perm (n, may be NULL).  d_work (m x n,
- * ld = m) receives the factored matrix if not NULL. */
+ * NULL), r (steps x n, may be NULL), perm (n, may be NULL). */
 IDK_API int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t steps,
                           double* d_q, double* d_r, int64_t* d_perm);
 

@@ -22,6 +22,11 @@ SIGNATURES = {
     "idk_last_error": (C.c_char_p, [_P]),
     "idk_status_string": (C.c_char_p, [C.c_int]),
     "idk_kernel_launches": (C.c_int64, [_P]),
+    "idk_set_profiling": (C.c_int, [_P, C.c_int]),
+    "idk_set_cpqr_mode": (C.c_int, [_P, C.c_int]),
+    "idk_debug_cpqr_trace": (C.c_int, [_P, _P]),
+    "idk_cpqr_plan": (C.c_int, [_P, _I64, _I64, _I64, C.POINTER(C.c_int64)]),
+    "idk_stage_times": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int]),
     "idk_optim_id": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "idk_sketch_rid": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _I64, _I64, C.c_uint64, C.c_int, _P, _P, _P, _P]),
     "idk_id_auto": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P, _P,

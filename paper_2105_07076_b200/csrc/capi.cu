@@ -35,6 +35,11 @@ struct idk_context {
     double* h_omega = nullptr;  // pinned staging for IDK_OMEGA_MT19937
     size_t h_omega_cap = 0;
     int64_t launches = 0;
+    int cpqr_mode = IDK_CPQR_AUTO;
+    // per-stage CUDA events on the launching stream (idk_set_profiling)
+    bool profiling = false;
+    cudaEvent_t ev[6] = {};
+    float stage_ms[5] = {};
 };
 
 namespace {
@@ -57,6 +62,24 @@ int cuda_fail(idk_context* h, cudaError_t e, const char* where) {
         cudaError_t _e = (call);                            \
         if (_e != cudaSuccess) return cuda_fail(h, _e, #call); \
     } while (0)
+
+// Stage boundaries: 0 input prep (Omega / copy), 1 sketch GEMM, 2 CPQR,
+// 3 R11 gather + TRSM (Z), 4 C gather.  mark(h, i) closes stage i-1.
+void mark(idk_context* h, int i) {
+    if (h->profiling) cudaEventRecord(h->ev[i], h->stream);
+}
+
+void collect_stage_times(idk_context* h) {
+    if (!h->profiling) return;
+    for (int i = 0; i < 5; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            ms = 0.f;
+        }
+        h->stage_ms[i] = ms;
+    }
+}
 
 // Grow-only buffer; growing synchronises the stream first (callers never
 // hold pointers across calls: every entry synchronises before returning).
@@ -92,27 +115,46 @@ int check_k(idk_context* h, int64_t m, int64_t n, int64_t k, const char* op) {
     return IDK_OK;
 }
 
-// Largest co-resident grid for the persistent CPQR kernel.
+// Largest co-resident grid for the streaming CPQR kernel.
 int cpqr_ctas(idk_context* h) { return h->num_sms; }
+
+// Which CPQR kernel runs an m' x n factorisation (see idk_set_cpqr_mode).
+struct CpqrChoice {
+    bool resident = false;
+    idk::ResidentPlan plan;
+};
+
+CpqrChoice choose_cpqr(idk_context* h, int64_t mrows, int64_t n, int64_t k) {
+    CpqrChoice c;
+    if (h->cpqr_mode == IDK_CPQR_STREAMING) return c;
+    c.plan = idk::cpqr_resident_plan(static_cast<int>(mrows), n, static_cast<int>(k), h->num_sms,
+                                     h->cpqr_mode != IDK_CPQR_RESIDENT_GRID);
+    cudaGetLastError();
+    c.resident = c.plan.ok;
+    return c;
+}
 
 // Work buffers of one CPQR + Z solve on an m' x n matrix.
 struct CpqrWs {
     size_t pos, pivots, taus, pub, barrier, r11, status;
 };
 
-CpqrWs carve_cpqr(Carve& cv, int64_t n, int64_t k, int num_sms) {
+CpqrWs carve_cpqr(Carve& cv, int64_t mrows, int64_t n, int64_t k, int num_sms, const CpqrChoice& ch) {
     CpqrWs w;
     w.pos = cv.take(sizeof(long long) * n);
     w.pivots = cv.take(sizeof(long long) * k);
     w.taus = cv.take(sizeof(double) * k);
-    w.pub = cv.take(idk::kCpqrPubBytes * 3 * static_cast<size_t>(num_sms + 1));
+    size_t pub = idk::kCpqrPubBytes * 3 * static_cast<size_t>(num_sms + 1);
+    if (ch.resident) pub = std::max(pub, idk::cpqr_resident_exchange_bytes(ch.plan, static_cast<int>(mrows)));
+    w.pub = cv.take(pub);
     w.barrier = cv.take(sizeof(unsigned));
     w.r11 = cv.take(sizeof(double) * k * k);
     w.status = cv.take(sizeof(int));
     return w;
 }
 
-int check_cpqr_fits(idk_context* h, int64_t mrows, int64_t n) {
+int check_cpqr_fits(idk_context* h, int64_t mrows, int64_t n, const CpqrChoice& ch) {
+    if (ch.resident) return IDK_OK;
     const int64_t G = std::min<int64_t>(n, h->num_sms);
     const int cols = static_cast<int>((n + G - 1) / G);
     if (idk::cpqr_smem_bytes(static_cast<int>(mrows), cols) > 200 * 1024)
@@ -122,27 +164,43 @@ int check_cpqr_fits(idk_context* h, int64_t mrows, int64_t n) {
     return IDK_OK;
 }
 
+cudaError_t run_cpqr(idk_context* h, const CpqrChoice& ch, double* W, int64_t mrows, int64_t n, int64_t k, char* base,
+                     const CpqrWs& w) {
+    long long* pos = reinterpret_cast<long long*>(base + w.pos);
+    long long* piv = reinterpret_cast<long long*>(base + w.pivots);
+    double* taus = reinterpret_cast<double*>(base + w.taus);
+    if (ch.resident)
+        return idk::cpqr_resident_launch(ch.plan, W, mrows, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv,
+                                         taus, base + w.pub, reinterpret_cast<unsigned*>(base + w.barrier), h->stream);
+    return idk::cpqr_launch(W, mrows, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
+                            reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream);
+}
+
 // CPQR(W) -> Z, C, cols; W is m' x n (ld m'), already resident and mutable.
-int factor_and_solve(idk_context* h, double* W, int64_t mrows, int64_t n, int64_t k, char* base, const CpqrWs& w,
-                     const double* d_a, int64_t lda, int64_t m_out, bool rows_of_a, int64_t* d_cols, double* d_z,
-                     double* d_c, bool det) {
+int factor_and_solve(idk_context* h, const CpqrChoice& ch, double* W, int64_t mrows, int64_t n, int64_t k, char* base,
+                     const CpqrWs& w, const double* d_a, int64_t lda, int64_t m_out, bool rows_of_a, int64_t* d_cols,
+                     double* d_z, double* d_c, bool det) {
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     double* taus = reinterpret_cast<double*>(base + w.taus);
     int* status = reinterpret_cast<int*>(base + w.status);
-    IDK_CUDA(idk::cpqr_launch(W, mrows, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
-                              reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream));
     IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
+    mark(h, 2);
+    IDK_CUDA(run_cpqr(h, ch, W, mrows, n, k, base, w));
+    mark(h, 3);
     IDK_CUDA(idk::id_solve_z(W, mrows, static_cast<int>(k), n, piv, pos, reinterpret_cast<double*>(base + w.r11),
                              status, d_z, h->stream));
+    mark(h, 4);
     h->launches += 3;
     if (d_c) {
         IDK_CUDA(idk::gather_columns(d_a, lda, m_out, piv, static_cast<int>(k), rows_of_a, d_c, h->stream));
         h->launches += 1;
     }
+    mark(h, 5);
     IDK_CUDA(cudaMemcpyAsync(d_cols, piv, sizeof(long long) * k, cudaMemcpyDeviceToDevice, h->stream));
     IDK_CUDA(cudaMemcpyAsync(h->h_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     IDK_CUDA(cudaStreamSynchronize(h->stream));
+    collect_stage_times(h);
     const int bad = *h->h_status;
     if (bad != 0x7f7f7f7f) {
         if (det)
@@ -161,12 +219,14 @@ int det_id(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda,
     if (rc) return rc;
     if (!d_a || !d_cols || !d_z) return set_err(h, IDK_ERR_INVALID_ARG, "optim_id: null pointer");
     if (lda < (trans ? n : m)) return set_err(h, IDK_ERR_INVALID_ARG, "optim_id: lda too small");
-    if ((rc = check_cpqr_fits(h, m, n))) return rc;
+    const CpqrChoice ch = choose_cpqr(h, m, n, k);
+    if ((rc = check_cpqr_fits(h, m, n, ch))) return rc;
     Carve cv;
     const size_t wofs = cv.take(sizeof(double) * m * n);
-    const CpqrWs w = carve_cpqr(cv, n, k, h->num_sms);
+    const CpqrWs w = carve_cpqr(cv, m, n, k, h->num_sms, ch);
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     double* W = reinterpret_cast<double*>(h->ws + wofs);
+    mark(h, 0);
     if (trans) {
         IDK_CUDA(idk::transpose_copy(d_a, lda, n, m, W, m, h->stream));
         h->launches += 1;
@@ -174,7 +234,8 @@ int det_id(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda,
         IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
                                    cudaMemcpyDeviceToDevice, h->stream));
     }
-    return factor_and_solve(h, W, m, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, true);
+    mark(h, 1);
+    return factor_and_solve(h, ch, W, m, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, true);
 }
 
 // Reference Box-Muller over mt19937_64 (random.cpp:10-15), column-major fill
@@ -201,15 +262,17 @@ int sketch_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t 
     if (omega_mode == IDK_OMEGA_VERBATIM && !d_omega)
         return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: verbatim omega requires d_omega");
     const int64_t l = k + p;
-    if ((rc = check_cpqr_fits(h, l, n))) return rc;
+    const CpqrChoice ch = choose_cpqr(h, l, n, k);
+    if ((rc = check_cpqr_fits(h, l, n, ch))) return rc;
     const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(l), n, m, h->num_sms);
     Carve cv;
     const size_t oofs = omega_mode == IDK_OMEGA_VERBATIM ? 0 : cv.take(sizeof(double) * l * m);
     const size_t yofs = cv.take(sizeof(double) * l * n);
     const size_t pofs = splits > 1 ? cv.take(sizeof(double) * l * n * splits) : 0;
-    const CpqrWs w = carve_cpqr(cv, n, k, h->num_sms);
+    const CpqrWs w = carve_cpqr(cv, l, n, k, h->num_sms, ch);
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     const double* omega = d_omega;
+    mark(h, 0);
     if (omega_mode != IDK_OMEGA_VERBATIM) {
         double* om = reinterpret_cast<double*>(h->ws + oofs);
         if (omega_mode == IDK_OMEGA_PHILOX) {
@@ -231,11 +294,12 @@ int sketch_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t 
         }
         omega = om;
     }
+    mark(h, 1);
     double* Y = reinterpret_cast<double*>(h->ws + yofs);
     IDK_CUDA(idk::sketch_gemm(omega, l, d_a, lda, trans, Y, l, static_cast<int>(l), n, m, splits,
                               splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr, h->stream));
     h->launches += splits > 1 ? 2 : 1;
-    return factor_and_solve(h, Y, l, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, false);
+    return factor_and_solve(h, ch, Y, l, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, false);
 }
 
 int id_auto_dev(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int method,
@@ -304,6 +368,8 @@ int idk_destroy(idk_handle h) {
     if (h->io) cudaFree(h->io);
     if (h->h_status) cudaFreeHost(h->h_status);
     if (h->h_omega) cudaFreeHost(h->h_omega);
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
     delete h;
     return IDK_OK;
 }
@@ -317,6 +383,49 @@ int idk_set_stream(idk_handle h, void* stream) {
 const char* idk_last_error(idk_handle h) { return h ? h->err.c_str() : "null handle"; }
 
 int64_t idk_kernel_launches(idk_handle h) { return h ? h->launches : 0; }
+
+int idk_set_cpqr_mode(idk_handle h, int mode) {
+    if (!h || mode < IDK_CPQR_AUTO || mode > IDK_CPQR_STREAMING) return IDK_ERR_INVALID_ARG;
+    h->cpqr_mode = mode;
+    return IDK_OK;
+}
+
+int idk_cpqr_plan(idk_handle h, int64_t m, int64_t n, int64_t k, int64_t* out8) {
+    if (!h || !out8) return IDK_ERR_INVALID_ARG;
+    const CpqrChoice c = choose_cpqr(h, m, n, k);
+    out8[0] = c.resident ? (c.plan.cluster ? 1 : 2) : 3;
+    out8[1] = c.plan.G;
+    out8[2] = c.plan.nc;
+    out8[3] = c.plan.S;
+    out8[4] = c.plan.R;
+    out8[5] = c.plan.l0;
+    out8[6] = c.plan.threads;
+    out8[7] = static_cast<int64_t>(c.plan.smem);
+    return IDK_OK;
+}
+
+// Debug: per-step phase clocks of the resident CPQR (CTA 0), k*8 int64 on device.
+int idk_debug_cpqr_trace(idk_handle h, int64_t* d_buf) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    idk::cpqr_resident_set_trace(reinterpret_cast<long long*>(d_buf));
+    return IDK_OK;
+}
+
+int idk_set_profiling(idk_handle h, int enable) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    if (enable && !h->ev[0]) {
+        for (auto& e : h->ev) IDK_CUDA(cudaEventCreate(&e));
+    }
+    h->profiling = enable != 0;
+    return IDK_OK;
+}
+
+int idk_stage_times(idk_handle h, double* ms_out, int max_stages) {
+    if (!h || !ms_out) return 0;
+    const int n = max_stages < 5 ? max_stages : 5;
+    for (int i = 0; i < n; ++i) ms_out[i] = h->stage_ms[i];
+    return n;
+}
 
 int idk_optim_id(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int64_t* d_cols,
                  double* d_z, double* d_c) {
@@ -401,12 +510,13 @@ int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n,
     if (m <= 0 || n <= 0 || steps < 1 || steps > std::min(m, n))
         return set_err(h, IDK_ERR_INVALID_ARG, "qr_column_pivoted: max_steps must lie in [1, min(rows, cols)]");
     if (lda < m) return set_err(h, IDK_ERR_INVALID_ARG, "qr_column_pivoted: lda too small");
-    int rc = check_cpqr_fits(h, m, n);
+    const CpqrChoice ch = choose_cpqr(h, m, n, steps);
+    int rc = check_cpqr_fits(h, m, n, ch);
     if (rc) return rc;
     Carve cv;
     const size_t wofs = cv.take(sizeof(double) * m * n);
     const size_t permofs = cv.take(sizeof(long long) * n);
-    const CpqrWs w = carve_cpqr(cv, n, steps, h->num_sms);
+    const CpqrWs w = carve_cpqr(cv, m, n, steps, h->num_sms, ch);
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     char* base = h->ws;
     double* W = reinterpret_cast<double*>(base + wofs);
@@ -415,8 +525,7 @@ int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n,
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     double* taus = reinterpret_cast<double*>(base + w.taus);
-    IDK_CUDA(idk::cpqr_launch(W, m, static_cast<int>(m), n, static_cast<int>(steps), pos, piv, taus, base + w.pub,
-                              reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream));
+    IDK_CUDA(run_cpqr(h, ch, W, m, n, steps, base, w));
     long long* perm = d_perm ? reinterpret_cast<long long*>(d_perm) : reinterpret_cast<long long*>(base + permofs);
     IDK_CUDA(idk::cpqr_finish(W, m, static_cast<int>(m), n, static_cast<int>(steps), pos, piv, taus, perm, d_r, d_q,
                               h->stream));

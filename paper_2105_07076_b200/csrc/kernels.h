@@ -24,6 +24,21 @@ cudaError_t cpqr_finish(const double* W, int64_t ldw, int m, int64_t n, int k, c
                         const long long* pivots, const double* taus, long long* perm, double* R, double* Q,
                         cudaStream_t stream);
 
+// cpqr_resident.cu
+struct ResidentPlan {
+    bool ok = false;
+    bool cluster = false;
+    int G = 0, nc = 0, S = 0, R = 0, l0 = 0, lds = 0, threads = 0;
+    size_t smem = 0;
+    double cost = 0;
+};
+ResidentPlan cpqr_resident_plan(int m, int64_t n, int k, int num_sms, bool allow_cluster);
+void cpqr_resident_set_trace(long long* device_buf);  // debug phase timing (nullptr = off)
+size_t cpqr_resident_exchange_bytes(const ResidentPlan& p, int m);
+cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, int m, int64_t n, int k,
+                                 long long* pos_out, long long* pivots, double* taus, void* exch, unsigned* barrier,
+                                 cudaStream_t stream);
+
 // trsm.cu
 int id_trsm_nb(int k);
 size_t id_trsm_smem_bytes(int k);

@@ -114,6 +114,29 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self.lib.idk_kernel_launches(self.h))
 
+    STAGES = ("prep", "sketch", "cpqr", "solve", "gather")
+    CPQR_AUTO, CPQR_RESIDENT_GRID, CPQR_STREAMING = 0, 1, 2
+
+    def set_cpqr_mode(self, mode: int):
+        self.check(self.lib.idk_set_cpqr_mode(self.h, mode))
+
+    def cpqr_plan(self, m: int, n: int, k: int) -> dict:
+        out = (C.c_int64 * 8)()
+        self.check(self.lib.idk_cpqr_plan(self.h, m, n, k, out))
+        kinds = {1: "cluster", 2: "resident-grid", 3: "streaming"}
+        keys = ("kind", "ctas", "cols_per_cta", "threads_per_col", "reg_rows", "smem_rows", "threads", "smem")
+        d = dict(zip(keys, list(out)))
+        d["kind"] = kinds[d["kind"]]
+        return d
+
+    def set_profiling(self, enable: bool = True):
+        self.check(self.lib.idk_set_profiling(self.h, 1 if enable else 0))
+
+    def stage_times(self) -> dict:
+        buf = (C.c_double * 5)()
+        n = self.lib.idk_stage_times(self.h, buf, 5)
+        return {self.STAGES[i]: buf[i] for i in range(n)}
+
 
 _tls = threading.local()
 

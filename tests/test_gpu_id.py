@@ -32,6 +32,15 @@ def idk():
     return idk
 
 
+@pytest.fixture(autouse=True, params=[0, 1, 2], ids=["cpqr-auto", "cpqr-resident-grid", "cpqr-streaming"])
+def cpqr_mode(request, idk):
+    """Every case runs on each CPQR kernel: cluster/resident (auto), resident grid, streaming."""
+    ctx = idk.context(0)
+    ctx.set_cpqr_mode(request.param)
+    yield request.param
+    ctx.set_cpqr_mode(0)
+
+
 def rel_error(a, c, z):
     return np.linalg.norm(a - c @ z) / np.linalg.norm(a)
 

@@ -27,6 +27,15 @@ def idk():
     return idk
 
 
+@pytest.fixture(autouse=True, params=[0, 1, 2], ids=["cpqr-auto", "cpqr-resident-grid", "cpqr-streaming"])
+def cpqr_mode(request, idk):
+    """Every case runs on each CPQR kernel: cluster/resident (auto), resident grid, streaming."""
+    ctx = idk.context(0)
+    ctx.set_cpqr_mode(request.param)
+    yield request.param
+    ctx.set_cpqr_mode(0)
+
+
 def qr(idk, a, steps):
     f = idk.qr_column_pivoted(dev(a), steps)
     return host(f.q), host(f.r), host(f.perm)
@@ -146,3 +155,24 @@ def test_exact_ties_break_to_lowest_position(idk, oracle):
         _, _, perm = qr(idk, a, k)
         _, _, rperm = oracle.qr_column_pivoted(a, k)
         assert np.array_equal(perm, rperm), n
+
+
+def test_planner_picks_on_chip_kernels(idk, cpqr_mode):
+    ctx = idk.context(0)
+    if cpqr_mode != 0:
+        pytest.skip("plan check runs once")
+    assert ctx.cpqr_plan(110, 4000, 100)["kind"] == "cluster"      # cfg2 sketch
+    assert ctx.cpqr_plan(500, 1000, 50)["kind"] == "cluster"       # cfg1
+    assert ctx.cpqr_plan(272, 16384, 256)["kind"] == "resident-grid"  # cfg4 sketch
+    assert ctx.cpqr_plan(72, 65536, 64)["kind"] == "resident-grid"    # cfg5 sketch
+
+
+@pytest.mark.parametrize("m,n,k", [(110, 4000, 100), (272, 16384, 256), (72, 65536, 64), (500, 1000, 50)])
+def test_config_shapes_match_oracle_qr(idk, oracle, m, n, k):
+    """Pivoted matrices with the BASELINE sketch shapes (random content): same pivots, R to rounding."""
+    rng = np.random.default_rng(m + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) * np.exp(-np.arange(n) / n)[None, :])
+    q, r, perm = qr(idk, a, k)
+    _, rr, rperm = oracle.qr_column_pivoted(a, k, want_q=False)
+    assert np.array_equal(perm, rperm)
+    assert rel(r, rr) <= 1e-12

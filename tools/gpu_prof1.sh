@@ -1,0 +1,6 @@
+python tools/prof_id.py cfg2 3 > gpurun_out/prof_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:cpqr_resident -s 1 -c 1 -o gpurun_out/prof_cpqr_cfg2 -f python tools/prof_id.py cfg2 3 > gpurun_out/ncu_cpqr.log 2>&1; echo ncu1 rc=$?
+python tools/prof_id.py cfg5 2 > gpurun_out/prof_plain5.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:cpqr_resident -s 1 -c 1 -o gpurun_out/prof_cpqr_cfg5 -f python tools/prof_id.py cfg5 2 > gpurun_out/ncu_cpqr5.log 2>&1; echo ncu2 rc=$?
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo ncu3 rc=$?

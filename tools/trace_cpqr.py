@@ -1,0 +1,56 @@
+"""Per-phase breakdown of the resident CPQR kernel from %globaltimer marks of
+every CTA: python tools/trace_cpqr.py cfg2 [mode]"""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2105_07076_b200 as idk  # noqa: E402
+from paper_2105_07076_b200.configs import CONFIGS, make_torch  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+mode = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+cfg = CONFIGS[name]
+a = make_torch(name, seed=20260601)
+ctx = idk.context(0)
+ctx.set_cpqr_mode(mode)
+mm = cfg.l if cfg.randomized else min(cfg.m, cfg.n)
+nn = max(cfg.m, cfg.n) if cfg.randomized else cfg.n
+plan = ctx.cpqr_plan(mm, nn, cfg.k)
+G, k = plan["ctas"], cfg.k
+buf = torch.zeros(G * (k + 1) * 8, dtype=torch.int64, device="cuda")
+for it in range(3):
+    ctx.lib.idk_debug_cpqr_trace(ctx.h, C.c_void_p(buf.data_ptr()) if it == 2 else None)
+    if cfg.randomized:
+        idk.id_auto(a, cfg.k, idk.RANDOMIZED, seed=1, p=cfg.p)
+    else:
+        idk.id_auto(a, cfg.k, idk.DETERMINISTIC)
+ctx.lib.idk_debug_cpqr_trace(ctx.h, None)
+t = buf.cpu().numpy().reshape(G, k + 1, 8).astype(np.float64)[:, :k, :]
+steps = k - 1
+names = ["update", "local argmax", "push cand+rec", "(unused)", "barrier", "select+copy", "->next top"]
+print(name, "mode", mode, "plan", plan)
+print(f"{'phase':20s} {'cta0 ns':>9s} {'mean ns':>9s} {'max ns':>9s}")
+for i, nm in enumerate(names):
+    if i == 3:
+        continue
+    if i == 4:
+        d = t[:, :steps, 5] - t[:, :steps, 3]
+    elif i < 6:
+        d = t[:, :steps, i + 1] - t[:, :steps, i]
+    else:
+        d = t[:, 1:steps + 1, 0] - t[:, :steps, 6]
+    print(f"{nm:20s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+for nm, (x, y) in [("  records loaded", (5, 4)), ("  reduce+sync", (4, 7)), ("  column copy", (7, 6))]:
+    d = t[:, :steps, y] - t[:, :steps, x]
+    print(f"{nm:20s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+arr = t[:, :steps, 3]
+print(f"arrival skew (max-min over CTAs of 'record written'): {(arr.max(0) - arr.min(0)).mean():.0f} ns")
+rel = t[:, :steps, 5]
+print(f"release skew (max-min of 'barrier done'): {(rel.max(0) - rel.min(0)).mean():.0f} ns; "
+      f"last arrival -> first release: {(rel.min(0) - t[:, :steps, 3].max(0)).mean():.0f} ns")
+tot = (t[0, 1:steps + 1, 0] - t[0, :steps, 0])
+print(f"step (cta0): mean {tot.mean():.0f} ns  first {tot[0]:.0f}  last {tot[-1]:.0f}")
