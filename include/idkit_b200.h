@@ -135,6 +135,15 @@ IDK_API int idk_id_auto(idk_handle h, const double* d_a, int64_t m, int64_t n, i
 IDK_API int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t m, int64_t n, int64_t lda,
                          int64_t stride, int64_t k, int64_t* d_cols, double* d_z, double* d_c);
 
+/* Sharded entry: the caller all-gathered the sketch Y
+ * (l x n, ldy) of a column-sharded A; factor it (CPQR, identical on every
+ * rank: deterministic) and solve Z only for its own columns [c_begin, c_end)
+ * into d_z_local (k x (c_end - c_begin), ld = k).  Y is overwritten with the
+ * factor.  cols = the k pivots (global column ids).  Collectives stay in the
+ * host layer (paper_2105_07076_b200/sharded.py, torch.distributed/NCCL). */
+IDK_API int idk_id_from_sketch(idk_handle h, double* d_y, int64_t l, int64_t n, int64_t ldy, int64_t k,
+                               int64_t c_begin, int64_t c_end, int64_t* d_cols, double* d_z_local);
+
 /* ---- stages / primitives (device pointers) ---------------------------------- */
 
 /* Omega (l x m, ld = l) = Philox Gaussian, keyed by seed (mirrors idko_omega_philox). */

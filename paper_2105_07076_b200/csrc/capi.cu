@@ -182,13 +182,12 @@ int factor_and_solve(idk_context* h, const CpqrChoice& ch, double* W, int64_t mr
                      double* d_z, double* d_c, bool det) {
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
-    double* taus = reinterpret_cast<double*>(base + w.taus);
     int* status = reinterpret_cast<int*>(base + w.status);
     IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
     mark(h, 2);
     IDK_CUDA(run_cpqr(h, ch, W, mrows, n, k, base, w));
     mark(h, 3);
-    IDK_CUDA(idk::id_solve_z(W, mrows, static_cast<int>(k), n, piv, pos, reinterpret_cast<double*>(base + w.r11),
+    IDK_CUDA(idk::id_solve_z(W, mrows, static_cast<int>(k), 0, n, piv, pos, reinterpret_cast<double*>(base + w.r11),
                              status, d_z, h->stream));
     mark(h, 4);
     h->launches += 3;
@@ -549,6 +548,40 @@ int idk_select_columns(idk_handle h, const double* d_a, int64_t m, int64_t n, in
     IDK_CUDA(idk::gather_columns(d_a, lda, rows_of_a ? n : m, reinterpret_cast<const long long*>(d_cols),
                                  static_cast<int>(ncols), rows_of_a != 0, d_out, h->stream));
     h->launches += 1;
+    return IDK_OK;
+}
+
+int idk_id_from_sketch(idk_handle h, double* d_y, int64_t l, int64_t n, int64_t ldy, int64_t k, int64_t c_begin,
+                       int64_t c_end, int64_t* d_cols, double* d_z_local) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    int rc = check_k(h, l, n, k, "id_from_sketch");
+    if (rc) return rc;
+    if (!d_y || !d_cols || (c_end > c_begin && !d_z_local) || ldy < l)
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_from_sketch: bad pointer or leading dimension");
+    if (c_begin < 0 || c_end < c_begin || c_end > n)
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_from_sketch: column range outside [0, n]");
+    const CpqrChoice ch = choose_cpqr(h, l, n, k);
+    if ((rc = check_cpqr_fits(h, l, n, ch))) return rc;
+    Carve cv;
+    const CpqrWs w = carve_cpqr(cv, l, n, k, h->num_sms, ch);
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    char* base = h->ws;
+    long long* pos = reinterpret_cast<long long*>(base + w.pos);
+    long long* piv = reinterpret_cast<long long*>(base + w.pivots);
+    int* status = reinterpret_cast<int*>(base + w.status);
+    IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
+    IDK_CUDA(run_cpqr(h, ch, d_y, l, n, k, base, w));
+    h->launches += 1;
+    // R11 + the local column range of Z only (columns are independent).
+    IDK_CUDA(idk::id_solve_z(d_y, ldy, static_cast<int>(k), c_begin, c_end - c_begin, piv, pos,
+                             reinterpret_cast<double*>(base + w.r11), status, d_z_local, h->stream));
+    h->launches += 2;
+    IDK_CUDA(cudaMemcpyAsync(d_cols, piv, sizeof(long long) * k, cudaMemcpyDeviceToDevice, h->stream));
+    IDK_CUDA(cudaMemcpyAsync(h->h_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    if (*h->h_status != 0x7f7f7f7f)
+        return set_err(h, IDK_ERR_SINGULAR, "solve_triangular: zero diagonal at index " + std::to_string(*h->h_status));
     return IDK_OK;
 }
 

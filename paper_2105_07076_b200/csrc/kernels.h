@@ -42,8 +42,8 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
 // trsm.cu
 int id_trsm_nb(int k);
 size_t id_trsm_smem_bytes(int k);
-cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t n, const long long* pivots, const long long* pos,
-                       double* R11, int* status, double* Z, cudaStream_t stream);
+cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int64_t n, const long long* pivots,
+                       const long long* pos, double* R11, int* status, double* Z, cudaStream_t stream);
 cudaError_t gather_columns(const double* A, int64_t lda, int64_t rows, const long long* cols, int k, bool rows_of_a,
                            double* C, cudaStream_t stream);
 cudaError_t copy_pivots(const long long* src, int k, long long* dst, cudaStream_t stream);

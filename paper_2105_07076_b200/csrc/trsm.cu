@@ -112,11 +112,16 @@ int id_trsm_nb(int k) {
 
 size_t id_trsm_smem_bytes(int k) { return sizeof(double) * static_cast<size_t>(id_trsm_nb(k)) * (k | 1); }
 
-cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t n, const long long* pivots, const long long* pos,
-                       double* R11, int* status, double* Z, cudaStream_t stream) {
+// Z[:, j] for the columns j in [c_begin, c_begin + n) of W (Z has ld k and
+// starts at column c_begin); R11 is gathered from the pivot columns of W.
+cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int64_t n, const long long* pivots,
+                       const long long* pos, double* R11, int* status, double* Z, cudaStream_t stream) {
     const int64_t kk = static_cast<int64_t>(k) * k;
     gather_r11_kernel<<<static_cast<int>(std::min<int64_t>((kk + 255) / 256, 1024)), 256, 0, stream>>>(
         W, ldw, pivots, k, R11, status);
+    W += c_begin * ldw;
+    pos += c_begin;
+    if (n <= 0) return cudaGetLastError();
     const size_t smem = id_trsm_smem_bytes(k);
     cudaError_t e = cudaFuncSetAttribute(id_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));

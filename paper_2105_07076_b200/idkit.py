@@ -273,6 +273,22 @@ def optim_id_batched(a, k: int, want_c: bool = True):
     return cols, z, c
 
 
+def id_from_sketch(y, k: int, c_begin: int = 0, c_end: Optional[int] = None):
+    """Factor an (all-gathered) sketch Y in place and solve Z for columns
+    [c_begin, c_end).  Returns (cols, z_local)."""
+    import torch
+    y = fortran(y)
+    l, n = y.shape
+    c_end = n if c_end is None else c_end
+    ctx = context(y.device.index or 0)
+    ctx.bind_stream()
+    cols = torch.empty(max(k, 0), dtype=torch.int64, device=y.device)
+    z = empty_f(max(k, 0), max(c_end - c_begin, 0), y.device)
+    ctx.check(ctx.lib.idk_id_from_sketch(ctx.h, _ptr(y), l, n, _ld(y), k, c_begin, c_end, _ptr(cols),
+                                         _ptr(z) if c_end > c_begin else None))
+    return cols, z
+
+
 # ---- stages / primitives ----------------------------------------------------------
 
 def sketch_omega(l: int, m: int, seed: int, device=0):
