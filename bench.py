@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--shard", action="store_true", help="cfg4/cfg5: use the sharded layer even at N=1")
     return ap.parse_args()
 
 
@@ -167,6 +168,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_2105_07076_b200 as idk
+    from paper_2105_07076_b200 import sharded
     from paper_2105_07076_b200.configs import CONFIGS, make_torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -177,27 +179,36 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
     dev = torch.device("cuda", local)
+    k, p = cfg.k, max(cfg.p, 0)
+    replicas = cfg.name in ("cfg1", "cfg2")       # too small to shard -> replicas only
+    use_sharded = (not replicas) and (world > 1 or args.shard) and cfg.name in ("cfg4", "cfg5")
 
     # ---- inputs (harness; not timed) ----
-    seed = args.seed + (rank if cfg.name in ("cfg1", "cfg2") else 0)
+    seed = args.seed + (rank if replicas else 0)
     a = make_torch(cfg.name, seed=seed, device=f"cuda:{local}")
-    if cfg.name == "cfg3" and world > 1:  # partition by matrix, no collective
-        per = (cfg.batch + world - 1) // world
-        a = a[rank * per:min(cfg.batch, (rank + 1) * per)].contiguous()
+    tall = cfg.m > cfg.n
+    n_dec = cfg.m if tall else cfg.n               # columns of the decomposed matrix M
+    begin, end = sharded.column_range(n_dec, world, rank) if use_sharded else (0, n_dec)
+    if cfg.name == "cfg3" and world > 1:           # partition by matrix, no collective
+        b3, e3 = sharded.batched_partition(cfg.batch, world, rank)
+        a = a[b3:e3].contiguous()
+    elif use_sharded:                              # this rank's block, stored contiguously
+        a = (a[begin:end, :] if tall else a[:, begin:end]).t().contiguous().t()
+    torch.cuda.empty_cache()
     ctx = idk.context(local)
     ctx.set_profiling(True)
-    k, p = cfg.k, max(cfg.p, 0)
+    stream = torch.cuda.current_stream(dev)
 
     def step():
         if cfg.name == "cfg3":
             return idk.optim_id_batched(a, k)
+        if use_sharded:
+            return sharded.sketch_rid_sharded(a, n_dec, k, p, seed=args.seed, transposed=tall)
         if cfg.randomized:
             return idk.id_auto(a, k, idk.RANDOMIZED, seed=args.seed, p=p)
         return idk.id_auto(a, k, idk.DETERMINISTIC)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize(dev)
@@ -217,35 +228,51 @@ def run_ours(args):
         starts[i].record(stream)
         step()
         ends[i].record(stream)
-        if cfg.name != "cfg3":
+        if cfg.name != "cfg3" and not use_sharded:
             for kname, v in ctx.stage_times().items():
                 stage_tot[kname] = stage_tot.get(kname, 0.0) + v
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     launches = ctx.kernel_launches - launches0
-    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    total_ms = sum(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends))
     clocks = sampler.stop()
 
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    total_ids = ids_per_step(cfg) * args.steps * (world if cfg.name != "cfg3" else 1)
-    if cfg.name == "cfg3" and world > 1:
-        total_ids = cfg.batch * args.steps
+    if replicas:
+        total_ids, scaling = world * args.steps, "weak"      # N independent replicas
+    elif cfg.name == "cfg3":
+        total_ids, scaling = cfg.batch * args.steps, "strong"  # the 4096-matrix batch split over N
+    else:
+        total_ids, scaling = args.steps, "strong"            # one sharded ID over N GPUs
     value = total_ids / (max_ms / 1e3)
 
     # ---- e2e through the public host-buffer API (H2D + compute + D2H each step) ----
     e2e = None
     if not args.no_e2e and cfg.name != "cfg3":
-        pinned = torch.empty((cfg.n, cfg.m), dtype=torch.float64).pin_memory()
+        pinned = torch.empty((a.shape[1], a.shape[0]), dtype=torch.float64).pin_memory()
         pinned.copy_(a.t().cpu())
-        ha = pinned.numpy().T  # F-ordered view of pinned memory
+        ha = pinned.numpy().T  # column-major view of pinned memory
         assert ha.flags["F_CONTIGUOUS"]
+        method = idk.RANDOMIZED if cfg.randomized else idk.DETERMINISTIC
+        zc = max(cfg.m, cfg.n)
+        crow = cfg.n if tall else cfg.m
+
+        def e2e_step():
+            if use_sharded:  # this rank's shard in from pinned memory, its Z block and C out
+                da = torch.empty_like(a)
+                da.copy_(pinned.t(), non_blocking=True)
+                cols, zl, c = sharded.sketch_rid_sharded(da, n_dec, k, p, seed=args.seed, transposed=tall)
+                cols.cpu(), zl.cpu(), c.cpu()
+                return
+            idk.id_auto(ha, k, method, seed=args.seed, p=p)
+
         ke = max(1, min(args.steps, 20))
         for _ in range(2):
-            idk.id_auto(ha, k, idk.RANDOMIZED if cfg.randomized else idk.DETERMINISTIC, seed=args.seed, p=p)
+            e2e_step()
         torch.cuda.synchronize(dev)
         ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
         ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
@@ -254,19 +281,23 @@ def run_ours(args):
         for i in range(ke):
             flush.zero_()
             ev0[i].record(stream)
-            r = idk.id_auto(ha, k, idk.RANDOMIZED if cfg.randomized else idk.DETERMINISTIC, seed=args.seed, p=p)
+            e2e_step()
             ev1[i].record(stream)
         torch.cuda.synchronize(dev)
         e_ms = torch.tensor([sum(x.elapsed_time(y) for x, y in zip(ev0, ev1))], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        zc = max(cfg.m, cfg.n)
-        crow = min(cfg.m, cfg.n) if cfg.m > cfg.n else cfg.m
-        e2e = {"value": world * ke / (float(e_ms.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": 8 * cfg.m * cfg.n,
-               "d2h_bytes_per_step": 8 * k + 8 * k * zc + 8 * crow * k,
-               "api": "idk_id_auto_host (include/idkit_b200.h), pinned host buffers"}
-        del r
+        ids = (world if replicas else 1) * ke
+        if use_sharded:
+            h2d = 8 * a.numel()
+            d2h = 8 * k + 8 * k * (end - begin) + 8 * crow * k
+        else:
+            h2d = 8 * cfg.m * cfg.n
+            d2h = 8 * k + 8 * k * zc + 8 * crow * k
+        e2e = {"value": ids / (float(e_ms.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "api": ("paper_2105_07076_b200.sharded.sketch_rid_sharded (per-rank shard, pinned host)" if use_sharded
+                       else "idk_id_auto_host (include/idkit_b200.h), pinned host buffers")}
 
     # ---- roofline of the dominant kernel ----
     peaks = load_json(PEAKS_FILE) or {"hbm_gbs": 6650.0, "_fallback": True}
@@ -275,8 +306,8 @@ def run_ours(args):
     ncu = load_json(NCU_SUMMARY) or {}
     roofline = None
     stage_avg = {}
-    if cfg.name != "cfg3" and stage_tot:
-        stage_avg = {s: v / args.steps for s, v in stage_tot.items()}
+    if stage_tot:
+        stage_avg = {s_: v / args.steps for s_, v in stage_tot.items()}
         dom = max(stage_avg, key=stage_avg.get)
         traffic = (ncu.get(cfg.name) or {}).get(dom, {}).get("dram_bytes_per_launch")
         roofline = roofline_for(dom, stage_work(cfg, cfg.n)[dom], stage_avg[dom], peaks, fp64, traffic)
@@ -295,15 +326,15 @@ def run_ours(args):
         cpu = cpu_baseline(cfg, a, args)
 
     if rank == 0:
+        par = ("replicas" if replicas else ("partition-by-matrix" if cfg.name == "cfg3" else
+                                            "column-sharded sketch + all_gather(Y)")) + f" x{world}"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded BASELINE construction (" + cfg.name + "), generated on device",
             "config": {"workload": workload_desc(cfg), "m": cfg.m, "n": cfg.n, "k": cfg.k, "p": cfg.p,
-                       "batch": cfg.batch,
-                       "parallelism": ("replicas" if cfg.name in ("cfg1", "cfg2") else "partition-by-matrix")
-                       + f" x{world}",
+                       "batch": cfg.batch, "parallelism": par,
                        "l2": "flushed between timed steps (256 MiB memset, outside the events)",
                        "inputs": "resident in HBM"},
             "stages_ms_per_step": stage_avg or None,
