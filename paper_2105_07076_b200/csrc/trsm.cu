@@ -85,6 +85,165 @@ id_trsm_kernel(const double* __restrict__ W, int64_t ldw, const double* __restri
     }
 }
 
+// Warp-independent back substitution (solve.cpp:43-51 restated): each warp
+// owns kCW right-hand sides with all k <= 32*KJ rows in registers (lane owns
+// rows lane + 32 j).  Step i broadcasts the finished x_i by shuffle, every lane
+// applies r_{.,i} x_i to its rows above i, and the owner of row i-1 finishes it
+// (multiplying by 1/r_{i-1,i-1}, computed once).  R11 column i-1 is loaded
+// while step i runs.  No block-level barrier anywhere.
+constexpr int kCW = 4;
+
+template <int KJ>
+__global__ void __launch_bounds__(128)
+id_trsm_warp_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ R11, int k, int64_t n,
+                    const long long* __restrict__ pos, double* __restrict__ Z) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t cbase = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wid) * kCW;
+    if (cbase >= n) return;
+    double x[kCW][KJ], rinv[KJ], rc[KJ], rn[KJ];
+#pragma unroll
+    for (int c = 0; c < kCW; ++c) {
+        const bool ok = cbase + c < n;
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+            const int row = lane + 32 * j;
+            x[c][j] = (ok && row < k) ? W[(cbase + c) * ldw + row] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) {
+        const int row = lane + 32 * j;
+        rinv[j] = row < k ? 1.0 / R11[static_cast<int64_t>(row) * k + row] : 0.0;
+    }
+    // row k-1 has no updates: finish it
+    {
+        const int jl = (k - 1) >> 5, tl = (k - 1) & 31;
+#pragma unroll
+        for (int j = 0; j < KJ; ++j)
+            if (j == jl && lane == tl)
+#pragma unroll
+                for (int c = 0; c < kCW; ++c) x[c][j] *= rinv[j];
+    }
+    // column k-1 of R11
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) {
+        const int row = lane + 32 * j;
+        rc[j] = row < k - 1 ? __ldg(R11 + static_cast<int64_t>(k - 1) * k + row) : 0.0;
+    }
+#pragma unroll
+    for (int j = KJ - 1; j >= 0; --j) {
+        const int tmax = min(31, k - 1 - 32 * j);
+        for (int t = tmax; t >= 0; --t) {
+            const int i = 32 * j + t;
+            if (i == 0) break;
+            // prefetch column i-1 (rows < i-1)
+#pragma unroll
+            for (int jr = 0; jr < KJ; ++jr) {
+                const int row = lane + 32 * jr;
+                rn[jr] = (jr <= j && row < i - 1) ? __ldg(R11 + static_cast<int64_t>(i - 1) * k + row) : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < kCW; ++c) {
+                const double xi = __shfl_sync(0xffffffffu, x[c][j], t);
+#pragma unroll
+                for (int jr = 0; jr < j; ++jr) x[c][jr] = fma(-rc[jr], xi, x[c][jr]);
+                if (lane < t) x[c][j] = fma(-rc[j], xi, x[c][j]);
+            }
+            // row i-1 is final now
+            if (t > 0) {
+                if (lane == t - 1)
+#pragma unroll
+                    for (int c = 0; c < kCW; ++c) x[c][j] *= rinv[j];
+            } else if (j > 0) {
+                if (lane == 31)
+#pragma unroll
+                    for (int c = 0; c < kCW; ++c) x[c][j - 1] *= rinv[j - 1];
+            }
+#pragma unroll
+            for (int jr = 0; jr < KJ; ++jr) rc[jr] = rn[jr];
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kCW; ++c) {
+        const int64_t col = cbase + c;
+        if (col >= n) break;
+        const long long p = pos[col];
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+            const int row = lane + 32 * j;
+            if (row < k) Z[col * k + row] = p < k ? (row == p ? 1.0 : 0.0) : x[c][j];
+        }
+    }
+}
+
+template <int KJ>
+cudaError_t launch_trsm_warp(const double* W, int64_t ldw, const double* R11, int k, int64_t n, const long long* pos,
+                             double* Z, cudaStream_t stream) {
+    const int64_t warps = (n + kCW - 1) / kCW;
+    const int64_t blocks = (warps + 3) / 4;
+    id_trsm_warp_kernel<KJ><<<static_cast<unsigned>(blocks), 128, 0, stream>>>(W, ldw, R11, k, n, pos, Z);
+    return cudaGetLastError();
+}
+
+// Right-looking back substitution over a k x NB tile of right-hand sides kept
+// in shared memory (solve.cpp:43-51 restated column-parallel): step i finishes
+// row i (the thread that applies the last update to x_i also divides by
+// r_ii), then every thread subtracts r_{.,i} x_i from the rows above.  One
+// __syncthreads per row; column i-1 of R11 is prefetched into shared memory
+// while step i runs.
+__global__ void __launch_bounds__(256)
+id_trsm_rl_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ R11, int k, int64_t n,
+                  const long long* __restrict__ pos, double* __restrict__ Z, int NB) {
+    extern __shared__ double sm[];
+    const int ldx = k | 1;
+    double* X = sm;                                   // NB columns, stride ldx
+    double* rcol = X + static_cast<size_t>(NB) * ldx;  // 2 x k: column i of R11 (double buffer)
+    double* rdiag = rcol + 2 * k;                     // k
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int lane = tid & 31, wid = tid >> 5, nw = T >> 5;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * NB;
+    const int nb = static_cast<int>(min(static_cast<long long>(NB), static_cast<long long>(n - c0)));
+
+    for (int c = wid; c < nb; c += nw)
+        for (int i = lane; i < k; i += 32) X[c * ldx + i] = W[(c0 + c) * ldw + i];
+    for (int i = tid; i < k; i += T) {
+        rdiag[i] = R11[static_cast<int64_t>(i) * k + i];
+        rcol[((k - 1) & 1) * k + i] = R11[static_cast<int64_t>(k - 1) * k + i];
+    }
+    __syncthreads();
+    // row k-1 has no updates: divide it
+    for (int c = tid; c < nb; c += T) X[c * ldx + k - 1] = X[c * ldx + k - 1] / rdiag[k - 1];
+    __syncthreads();
+    for (int i = k - 1; i > 0; --i) {
+        const double* rc = rcol + (i & 1) * k;  // R11[0:i, i]
+        // prefetch column i-1 for the next step (async copy: no stall on L2 latency)
+        double* rn = rcol + ((i - 1) & 1) * k;
+        for (int r = tid; r < i - 1; r += T) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(rn + r));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                         "l"(R11 + static_cast<int64_t>(i - 1) * k + r));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        // warp w owns columns w, w+nw, ...; lane owns rows lane, lane+32, ... (< i)
+        for (int c = wid; c < nb; c += nw) {
+            double* xc = X + c * ldx;
+            const double xi = xc[i];
+            for (int r = lane; r < i; r += 32) {
+                double v = fma(-rc[r], xi, xc[r]);
+                if (r == i - 1) v = v / rdiag[r];  // x_{i-1} is final now
+                xc[r] = v;
+            }
+        }
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+    }
+    for (int c = wid; c < nb; c += nw) {
+        const int64_t col = c0 + c;
+        const long long p = pos[col];
+        for (int i = lane; i < k; i += 32) Z[col * k + i] = p < k ? (i == p ? 1.0 : 0.0) : X[c * ldx + i];
+    }
+}
+
 // C[:, j] = A[:, cols[j]]  (matrix.cpp:121-130), or for the id_auto dual
 // C[:, j] = A[cols[j], :]^T (a row of the tall A is a column of A^T).
 __global__ void gather_columns_kernel(const double* __restrict__ A, int64_t lda, int64_t rows,
@@ -122,13 +281,40 @@ cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int
     W += c_begin * ldw;
     pos += c_begin;
     if (n <= 0) return cudaGetLastError();
+    switch ((k + 31) / 32) {
+        case 1: return launch_trsm_warp<1>(W, ldw, R11, k, n, pos, Z, stream);
+        case 2: return launch_trsm_warp<2>(W, ldw, R11, k, n, pos, Z, stream);
+        case 3: return launch_trsm_warp<3>(W, ldw, R11, k, n, pos, Z, stream);
+        case 4: return launch_trsm_warp<4>(W, ldw, R11, k, n, pos, Z, stream);
+        case 5: return launch_trsm_warp<5>(W, ldw, R11, k, n, pos, Z, stream);
+        case 6: return launch_trsm_warp<6>(W, ldw, R11, k, n, pos, Z, stream);
+        case 7: return launch_trsm_warp<7>(W, ldw, R11, k, n, pos, Z, stream);
+        case 8: return launch_trsm_warp<8>(W, ldw, R11, k, n, pos, Z, stream);
+        default: break;  // k > 256: shared-memory kernels below
+    }
+    // Right-hand sides per CTA: enough CTAs to cover the SMs twice, at most 64,
+    // and the k x NB tile within ~150 KB of shared memory.
+    int nb = static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(8, n / 296)));
+    nb = (nb + 7) & ~7;
+    while (nb > 1 && sizeof(double) * (static_cast<size_t>(nb) * (k | 1) + 3 * static_cast<size_t>(k)) > 150 * 1024)
+        nb = nb > 8 ? nb - 8 : nb - 1;
+    if (sizeof(double) * (static_cast<size_t>(nb) * (k | 1) + 3 * static_cast<size_t>(k)) <= 200 * 1024) {
+        const size_t smem = sizeof(double) * (static_cast<size_t>(nb) * (k | 1) + 3 * static_cast<size_t>(k));
+        cudaError_t e = cudaFuncSetAttribute(id_trsm_rl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const int64_t blocks = (n + nb - 1) / nb;
+        id_trsm_rl_kernel<<<static_cast<unsigned>(blocks), 256, smem, stream>>>(W, ldw, R11, k, n, pos, Z, nb);
+        return cudaGetLastError();
+    }
+    // very large k: blocked kernel with global R11 reads
     const size_t smem = id_trsm_smem_bytes(k);
     cudaError_t e = cudaFuncSetAttribute(id_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const int nb = id_trsm_nb(k);
-    const int64_t blocks = (n + nb - 1) / nb;
-    id_trsm_kernel<<<static_cast<unsigned>(blocks), kTrsmThreads, smem, stream>>>(W, ldw, R11, k, n, pos, Z, nb);
+    const int nb2 = id_trsm_nb(k);
+    const int64_t blocks = (n + nb2 - 1) / nb2;
+    id_trsm_kernel<<<static_cast<unsigned>(blocks), kTrsmThreads, smem, stream>>>(W, ldw, R11, k, n, pos, Z, nb2);
     return cudaGetLastError();
 }
 
