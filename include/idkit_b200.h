@@ -79,6 +79,10 @@ IDK_API const char* idk_status_string(int status);
 IDK_API int64_t idk_kernel_launches(idk_handle h);
 /* Select the CPQR kernel (idk_cpqr_mode); default IDK_CPQR_AUTO. */
 IDK_API int idk_set_cpqr_mode(idk_handle h, int mode);
+/* Batched entry: 1 = the bit-identical kernel (reference summation order,
+ * unfused IEEE ops); 0 (default) = the throughput kernel (registers + TMA
+ * prefetch + FMA), which matches within rounding. */
+IDK_API int idk_set_batched_exact(idk_handle h, int exact);
 /* The CPQR plan for an m x n, k-step factorisation: out8 = {kind (1 cluster,
  * 2 resident grid, 3 streaming), CTAs, columns per CTA, threads per column,
  * register rows per thread, shared-memory rows, threads per CTA, smem bytes}. */
@@ -127,9 +131,12 @@ IDK_API int idk_id_auto(idk_handle h, const double* d_a, int64_t m, int64_t n, i
 
 /* Batched deterministic ID (BASELINE cfg3): batch independent m x n
  * matrices at d_a + b*stride (lda each), one CTA per matrix, outputs packed:
- * cols b*k, Z b*k*n, C b*m*k.  Bit-identical to the reference composition
- * qr_column_pivoted -> solve_triangular -> select_columns per matrix.
- * Needs m*n small enough for shared memory (64 x 256 uses 139 KB).  A zero
+ * cols b*k, Z b*k*n, C b*m*k.  Default kernel: persistent CTAs, one thread
+ * per column in registers, next matrix prefetched by TMA bulk copies (m <= 64,
+ * n <= 256, k <= 32); with idk_set_batched_exact(h, 1) (or other shapes)
+ * the kernel that is bit-identical to the reference composition
+ * qr_column_pivoted -> solve_triangular -> select_columns per matrix runs
+ * (needs m*n in shared memory: 64 x 256 uses 139 KB).  A zero
  * |r_ii| in any matrix -> IDK_ERR_NOT_POSDEF (first failing batch index in
  * the message). */
 IDK_API int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t m, int64_t n, int64_t lda,

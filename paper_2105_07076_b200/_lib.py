@@ -24,6 +24,7 @@ SIGNATURES = {
     "idk_kernel_launches": (C.c_int64, [_P]),
     "idk_set_profiling": (C.c_int, [_P, C.c_int]),
     "idk_set_cpqr_mode": (C.c_int, [_P, C.c_int]),
+    "idk_set_batched_exact": (C.c_int, [_P, C.c_int]),
     "idk_debug_cpqr_trace": (C.c_int, [_P, _P]),
     "idk_cpqr_plan": (C.c_int, [_P, _I64, _I64, _I64, C.POINTER(C.c_int64)]),
     "idk_stage_times": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int]),

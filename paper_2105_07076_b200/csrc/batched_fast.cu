@@ -1,0 +1,371 @@
+// batched_fast.cu -- many small IDs (BASELINE cfg3), one persistent CTA per SM.
+//
+// Same algorithm as batched.cu (the reference's CPQR qr.cpp:42-126, the
+// triangular solve solve.cpp:23-53 and the gather matrix.cpp:121-130 per
+// matrix), organised for throughput instead of bit-identity:
+//   * one thread per column, the column's m <= M rows held in registers;
+//   * the next matrix streams into shared memory by TMA bulk copies
+//     (cp.async.bulk + mbarrier) while the current one is factored, so HBM
+//     traffic overlaps the FP64 work;
+//   * FMA arithmetic and the reflector's v kept in shared memory between zero
+//     guard rows, so the update loops have no predicates;
+//   * the pivot rule is exact (lowest position among sqrt(live) >=
+//     (1-1e-14) sqrt(max)); positions replay the reference's swaps;
+//   * Z is staged in shared memory and written coalesced.
+// Results match the reference within rounding (tests use identical columns
+// and ||dZ||/||Z|| <= 1e-10); batched.cu remains the bit-identical kernel.
+#include <climits>
+
+#include "common.cuh"
+
+namespace idk {
+
+namespace {
+
+constexpr int kFastThreads = 256;  // max columns (2 threads each)
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(a),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s),
+                 "l"(gmem), "r"(bytes), "r"(b)
+                 : "memory");
+}
+
+// Warp max of non-negative doubles (-1 = none) via two 32-bit redux.sync.
+__device__ __forceinline__ double wmax_nonneg(double v) {
+    const bool has = v >= 0.0;
+    const unsigned long long b = has ? static_cast<unsigned long long>(__double_as_longlong(v)) + 1ull : 0ull;
+    const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(b >> 32));
+    const unsigned lo = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(b >> 32) == hi ? static_cast<unsigned>(b) : 0u);
+    const unsigned long long r = (static_cast<unsigned long long>(hi) << 32) | lo;
+    return r == 0ull ? -1.0 : __longlong_as_double(static_cast<long long>(r - 1ull));
+}
+
+__device__ __forceinline__ bool tie_ok(double v, double vmax) {  // qr.cpp:71-73, exact
+    if (v == vmax) return true;
+    if (!(v >= vmax * (1.0 - 4e-14))) return false;
+    return sqrt(v) >= (1.0 - 1e-14) * sqrt(vmax);
+}
+
+#define IDK_REP64_UNUSED(M)                                                                                  \
+    M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16) M(17) \
+    M(18) M(19) M(20) M(21) M(22) M(23) M(24) M(25) M(26) M(27) M(28) M(29) M(30) M(31) M(32) M(33)   \
+    M(34) M(35) M(36) M(37) M(38) M(39) M(40) M(41) M(42) M(43) M(44) M(45) M(46) M(47) M(48) M(49)   \
+    M(50) M(51) M(52) M(53) M(54) M(55) M(56) M(57) M(58) M(59) M(60) M(61) M(62) M(63)
+
+}  // namespace
+
+// Shared-memory load the compiler may not hoist: keeps the number of reflector
+// values in flight bounded (8 per chunk) instead of spilling the register-
+// resident column.
+__device__ __forceinline__ double lds_v(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+    return v;
+}
+
+// Trailing update of one non-pivot column at compile-time step S: dot with v
+// (rows S..M-1), axpy, downdate, recompute, next-step partials -- every loop
+// has static bounds, so no predicates and no retired rows are touched.  The
+// reflector values are read 8 at a time (lds_v) so the register-resident
+// column is not spilled.
+template <int M, int S>
+__device__ __forceinline__ void column_step(double (&y)[M], const double* __restrict__ vfull, double tau,
+                                            double& live, double& anchor, double& pa, double& pt) {
+    const double ys = y[S];
+    double head = ys;
+    if (tau != 0.0) {
+        double d0 = ys, d1 = 0.0, d2 = 0.0, d3 = 0.0;  // v_S = 1
+#pragma unroll
+        for (int i0 = S + 1; i0 < M; i0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u < M) v[u] = lds_v(vfull + i0 + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (i0 + u < M) {
+                    if ((u & 3) == 0) d0 = fma(v[u], y[i0 + u], d0);
+                    else if ((u & 3) == 1) d1 = fma(v[u], y[i0 + u], d1);
+                    else if ((u & 3) == 2) d2 = fma(v[u], y[i0 + u], d2);
+                    else d3 = fma(v[u], y[i0 + u], d3);
+                }
+            }
+        }
+        const double w = mul_rn((d0 + d1) + (d2 + d3), tau);
+        y[S] = ys - w;
+#pragma unroll
+        for (int i0 = S + 1; i0 < M; i0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u < M) v[u] = lds_v(vfull + i0 + u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u < M) y[i0 + u] = fma(-w, v[u], y[i0 + u]);
+        }
+        head = ys - w;
+    }
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int i = S + 2; i < M; ++i) {
+        if (i & 1) t1 = fma(y[i], y[i], t1);
+        else t0 = fma(y[i], y[i], t0);
+    }
+    pa = S + 1 < M ? y[S + 1 < M ? S + 1 : 0] : 0.0;
+    pt = t0 + t1;
+    double lv = sub_rn(live, mul_rn(head, head));
+    if (lv < 0.0) lv = 0.0;
+    if (lv <= mul_rn(1e-6, anchor)) {  // qr.cpp:100-104
+        lv = fma(pa, pa, pt);
+        anchor = lv;
+    }
+    live = lv;
+}
+
+// The pivot column becomes [R; beta; v] (the reference's work layout).
+template <int M, int S>
+__device__ __forceinline__ void pivot_step(double (&y)[M], const double* __restrict__ vfull, double tau, double beta) {
+    if (tau != 0.0) {
+        y[S] = beta;
+#pragma unroll
+        for (int i = S + 1; i < M; ++i) y[i] = vfull[i];
+    }
+}
+
+#define IDK_REP32(M) \
+    M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) \
+    M(16) M(17) M(18) M(19) M(20) M(21) M(22) M(23) M(24) M(25) M(26) M(27) M(28) M(29) M(30) M(31)
+
+template <int M, int KM>
+__global__ void __launch_bounds__(kFastThreads, 1)
+batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
+                    long long* __restrict__ cols_out, double* __restrict__ Z, double* __restrict__ C,
+                    int* __restrict__ status) {
+    constexpr int LDS = M + 2;  // 16-byte aligned column stride; lane stride 2 banks apart
+    extern __shared__ __align__(128) double sm[];
+    double* stage = sm;                                   // n * LDS (TMA target)
+    double* colbuf = stage + static_cast<size_t>(n) * LDS;  // M: the pivot column as it stands
+    double* vfull = colbuf + M;                           // M: reflector by row (0 above s, 1 at s)
+    double* r11 = vfull + M;                              // KM x KM, column-major
+    double* zst = r11 + KM * KM;                          // k * n staging for Z
+    __shared__ uint64_t bar;
+    __shared__ double red_d[8];
+    __shared__ unsigned red_u[8];
+    __shared__ double s_pa, s_sc[3];
+    __shared__ int s_piv[KM];
+    __shared__ int s_ppos;
+
+    const int c = threadIdx.x, lane = c & 31, wid = c >> 5;
+    const bool mine = c < n;
+    if (c == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto prefetch = [&](int64_t b) {
+        if (wid == 0 && b < batch) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of stage
+            if (lane == 0) mbar_expect_tx(&bar, static_cast<unsigned>(n) * m * 8u);
+            __syncwarp();
+            const double* src = A + b * stride;
+            for (int j = lane; j < n; j += 32) bulk_g2s(stage + static_cast<size_t>(j) * LDS, src + j * lda, m * 8u, &bar);
+        }
+    };
+
+    unsigned phase = 0;
+    prefetch(blockIdx.x);
+    for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        double y[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) y[i] = (mine && i < m) ? stage[c * LDS + i] : 0.0;
+        __syncthreads();
+        prefetch(b + gridDim.x);  // next matrix streams in while this one is factored
+
+        // norms (qr.cpp:56-62) and the first reflector's inputs
+        double live, anchor, pa = y[0], pt;
+        {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int i = 1; i < M; ++i) {
+                if (i & 1) s1 = fma(y[i], y[i], s1);
+                else s0 = fma(y[i], y[i], s0);
+            }
+            pt = s0 + s1;
+            live = anchor = fma(y[0], y[0], pt);
+        }
+        int pos = c;
+
+        for (int s = 0; s < k; ++s) {
+            // ---- pivot: max live, then the lowest qualifying position (qr.cpp:66-78) ----
+            const bool cand = mine && pos >= s;
+            double mx = wmax_nonneg(cand ? live : -1.0);
+            if (lane == 0) red_d[wid] = mx;
+            __syncthreads();
+            mx = wmax_nonneg(lane < kFastThreads / 32 ? red_d[lane] : -1.0);
+            const unsigned key = (cand && tie_ok(live, mx)) ? static_cast<unsigned>(pos) : 0xffffffffu;
+            const unsigned wmin = __reduce_min_sync(0xffffffffu, key);
+            if (lane == 0) red_u[wid] = wmin;
+            __syncthreads();
+            const unsigned best = __reduce_min_sync(0xffffffffu, lane < kFastThreads / 32 ? red_u[lane] : 0xffffffffu);
+            const bool piv = mine && static_cast<unsigned>(pos) == best;
+            if (piv) {  // publish the pivot column and its reflector (qr.cpp:16-28)
+#pragma unroll
+                for (int i = 0; i < M; ++i) colbuf[i] = y[i];
+                const int len = m - s;
+                double tau = 0.0, beta = pa, scale = 1.0;
+                if (len > 1 && pt != 0.0) {
+                    beta = -copysign(sqrt(add_rn(mul_rn(pa, pa), pt)), pa);
+                    tau = (beta - pa) / beta;
+                    scale = 1.0 / (pa - beta);
+                }
+                s_pa = pa;
+                s_sc[0] = tau;
+                s_sc[1] = beta;
+                s_sc[2] = scale;
+                s_piv[s] = c;
+                s_ppos = pos;
+            }
+            __syncthreads();
+            const double alpha = s_pa, tau = s_sc[0], beta = s_sc[1], scale = s_sc[2];
+            if (c < M) {
+                const double v = c < s ? 0.0 : (c == s ? 1.0 : (c < m ? (tau != 0.0 ? mul_rn(colbuf[c], scale)
+                                                                                    : colbuf[c]) : 0.0));
+                vfull[c] = v;
+                if (c < KM && c <= s) r11[s * KM + c] = c < s ? colbuf[c] : (tau != 0.0 ? beta : alpha);
+            }
+            if (mine && !piv && pos == s) pos = s_ppos;  // the column at position s takes the pivot's place
+            if (piv) pos = s;
+            __syncthreads();
+            // ---- trailing update + downdate (qr.cpp:93-106), step-specialised ----
+            if (mine) {
+                if (piv) {
+                    switch (s) {
+#define IDK_PIV_CASE(r) \
+    case r:             \
+        if constexpr (r < M) pivot_step<M, (r < M ? r : 0)>(y, vfull, tau, beta); \
+        break;
+                        IDK_REP32(IDK_PIV_CASE)
+#undef IDK_PIV_CASE
+                        default:
+                            break;
+                    }
+                } else if (pos > s) {
+                    switch (s) {
+#define IDK_COL_CASE(r) \
+    case r:             \
+        if constexpr (r < M) column_step<M, (r < M ? r : 0)>(y, vfull, tau, live, anchor, pa, pt); \
+        break;
+                        IDK_REP32(IDK_COL_CASE)
+#undef IDK_COL_CASE
+                        default:
+                            break;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- T = R11^-1 R12 per column (solve.cpp:43-51), Z staged in smem ----
+        if (mine) {
+            if (pos >= k) {
+#pragma unroll
+                for (int i = KM - 1; i >= 0; --i) {
+                    if (i < k) {
+                        double acc = y[i];
+#pragma unroll
+                        for (int l = i + 1; l < KM; ++l)
+                            if (l < k) acc = fma(-r11[l * KM + i], y[l], acc);
+                        y[i] = acc / r11[i * KM + i];
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < KM; ++i)
+                if (i < k) zst[c * k + i] = pos < k ? (i == pos ? 1.0 : 0.0) : y[i];
+        }
+        if (c == 0) {
+            int bad = -1;
+            for (int i = 0; i < k; ++i)
+                if (fabs(r11[i * KM + i]) <= 1e-300) {
+                    bad = i;
+                    break;
+                }
+            status[b] = bad;
+        }
+        __syncthreads();
+        double* Zb = Z + b * static_cast<int64_t>(k) * n;
+        for (int e = c; e < k * n; e += kFastThreads) Zb[e] = zst[e];
+        long long* cb = cols_out + b * k;
+        for (int j = c; j < k; j += kFastThreads) cb[j] = s_piv[j];
+        if (C) {
+            const double* Ab = A + b * stride;
+            double* Cb = C + b * static_cast<int64_t>(m) * k;
+            for (int e = c; e < m * k; e += kFastThreads) {
+                const int j = e / m, i = e - j * m;
+                Cb[e] = Ab[static_cast<int64_t>(s_piv[j]) * lda + i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+size_t batched_fast_smem_bytes(int n, int k) {
+    const int M = 64, KM = k <= 16 ? 16 : 32;
+    return sizeof(double) * (static_cast<size_t>(n) * (M + 2) + 2 * M + KM * KM + static_cast<size_t>(k) * n);
+}
+
+bool batched_fast_ok(const double* A, int64_t lda, int64_t stride, int m, int n, int k, size_t smem_optin) {
+    return m <= 64 && m % 2 == 0 && n <= kFastThreads && k <= 32 && lda % 2 == 0 && stride % 2 == 0 &&
+           (reinterpret_cast<uintptr_t>(A) & 15) == 0 && batched_fast_smem_bytes(n, k) <= smem_optin;
+}
+
+cudaError_t batched_id_fast(const double* A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
+                            long long* cols, double* Z, double* C, int* status, int num_sms, cudaStream_t stream) {
+    if (batch <= 0) return cudaSuccess;
+    const size_t smem = batched_fast_smem_bytes(n, k);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(batch, num_sms));
+    if (k <= 16) {
+        auto kern = batched_fast_kernel<64, 16>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kFastThreads, smem, stream>>>(A, lda, stride, batch, m, n, k, cols, Z, C, status);
+    } else {
+        auto kern = batched_fast_kernel<64, 32>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kFastThreads, smem, stream>>>(A, lda, stride, batch, m, n, k, cols, Z, C, status);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace idk

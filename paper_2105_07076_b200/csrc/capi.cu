@@ -36,6 +36,7 @@ struct idk_context {
     size_t h_omega_cap = 0;
     int64_t launches = 0;
     int cpqr_mode = IDK_CPQR_AUTO;
+    bool batched_exact = false;
     // per-stage CUDA events on the launching stream (idk_set_profiling)
     bool profiling = false;
     cudaEvent_t ev[6] = {};
@@ -389,6 +390,12 @@ int idk_set_cpqr_mode(idk_handle h, int mode) {
     return IDK_OK;
 }
 
+int idk_set_batched_exact(idk_handle h, int exact) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    h->batched_exact = exact != 0;
+    return IDK_OK;
+}
+
 int idk_cpqr_plan(idk_handle h, int64_t m, int64_t n, int64_t k, int64_t* out8) {
     if (!h || !out8) return IDK_ERR_INVALID_ARG;
     const CpqrChoice c = choose_cpqr(h, m, n, k);
@@ -457,15 +464,23 @@ int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t
     int rc = check_k(h, m, n, k, "optim_id_batched");
     if (rc) return rc;
     if (lda < m || stride < lda * n) return set_err(h, IDK_ERR_INVALID_ARG, "optim_id_batched: bad lda/stride");
-    if (idk::batched_id_smem_bytes(static_cast<int>(m), static_cast<int>(n)) > h->smem_optin)
+    const bool fast = !h->batched_exact && idk::batched_fast_ok(d_a, lda, stride, static_cast<int>(m),
+                                                                 static_cast<int>(n), static_cast<int>(k), h->smem_optin);
+    if (!fast && idk::batched_id_smem_bytes(static_cast<int>(m), static_cast<int>(n)) > h->smem_optin)
         return set_err(h, IDK_ERR_INVALID_ARG, "optim_id_batched: m x n too large for one CTA's shared memory");
     if (batch == 0) return IDK_OK;
     Carve cv;
     const size_t sofs = cv.take(sizeof(int) * batch);
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     int* status = reinterpret_cast<int*>(h->ws + sofs);
-    IDK_CUDA(idk::batched_id(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
-                             reinterpret_cast<long long*>(d_cols), d_z, d_c, status, h->stream));
+    if (fast)
+        IDK_CUDA(idk::batched_id_fast(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n),
+                                      static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
+                                      h->num_sms, h->stream));
+    else
+        IDK_CUDA(idk::batched_id(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n),
+                                 static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
+                                 h->stream));
     h->launches += 1;
     std::vector<int> st(static_cast<size_t>(batch));
     IDK_CUDA(cudaMemcpyAsync(st.data(), status, sizeof(int) * batch, cudaMemcpyDeviceToHost, h->stream));

@@ -53,6 +53,12 @@ size_t batched_id_smem_bytes(int m, int n);
 cudaError_t batched_id(const double* A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
                        long long* cols, double* Z, double* C, int* status, cudaStream_t stream);
 
+// batched_fast.cu
+size_t batched_fast_smem_bytes(int n, int k);
+bool batched_fast_ok(const double* A, int64_t lda, int64_t stride, int m, int n, int k, size_t smem_optin);
+cudaError_t batched_id_fast(const double* A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
+                            long long* cols, double* Z, double* C, int* status, int num_sms, cudaStream_t stream);
+
 // util.cu
 cudaError_t transpose_copy(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb,
                            cudaStream_t stream);

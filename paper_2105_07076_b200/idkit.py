@@ -120,6 +120,9 @@ class Context:
     def set_cpqr_mode(self, mode: int):
         self.check(self.lib.idk_set_cpqr_mode(self.h, mode))
 
+    def set_batched_exact(self, exact: bool = True):
+        self.check(self.lib.idk_set_batched_exact(self.h, 1 if exact else 0))
+
     def cpqr_plan(self, m: int, n: int, k: int) -> dict:
         out = (C.c_int64 * 8)()
         self.check(self.lib.idk_cpqr_plan(self.h, m, n, k, out))

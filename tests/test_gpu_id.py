@@ -249,7 +249,12 @@ def test_batched_bit_identical_to_reference_composition(idk, ref):
     batch, m, n, k = 37, 64, 256, 16
     from paper_2105_07076_b200.configs import low_rank_batch_np
     a = low_rank_batch_np(batch, m, n, 16, 1e-4, 3)
-    cols, z, c = idk.optim_id_batched(torch.from_numpy(a).cuda(), k)
+    ctx = idk.context(0)
+    ctx.set_batched_exact(True)
+    try:
+        cols, z, c = idk.optim_id_batched(torch.from_numpy(a).cuda(), k)
+    finally:
+        ctx.set_batched_exact(False)
     cols, z, c = host(cols), host(z), host(c)
     for b in range(batch):
         ab = np.asfortranarray(a[b].T)
@@ -261,6 +266,23 @@ def test_batched_bit_identical_to_reference_composition(idk, ref):
             ocols, oz, _ = ref.optim_id(ab, k)
             assert np.array_equal(cols[b], ocols)
             assert rel(z[b].T, oz) <= ZTOL
+
+
+@pytest.mark.parametrize("batch,m,n,k,noise", [(300, 64, 256, 16, 1e-4), (57, 64, 256, 16, 1e-8), (40, 48, 200, 12, 1e-3),
+                                               (33, 64, 128, 32, 1e-2), (20, 20, 60, 5, 1e-4)])
+def test_batched_fast_matches_reference(idk, ref, batch, m, n, k, noise):
+    """Throughput kernel (default): identical columns, Z within 1e-10, C exact."""
+    import torch
+    from paper_2105_07076_b200.configs import low_rank_batch_np
+    a = low_rank_batch_np(batch, m, n, k, noise, 5)
+    cols, z, c = idk.optim_id_batched(torch.from_numpy(a).cuda(), k)
+    cols, z, c = host(cols), host(z), host(c)
+    for b in range(batch):
+        ab = np.asfortranarray(a[b].T)
+        rcols, rz, rc = ref.sketch_id(ab, k, None)
+        assert np.array_equal(cols[b], rcols), b
+        assert rel(z[b].T, rz) <= ZTOL, b
+        assert np.array_equal(c[b].T, rc), b
 
 
 def test_batched_rank_deficient_raises(idk):
