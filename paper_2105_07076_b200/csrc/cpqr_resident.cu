@@ -28,6 +28,7 @@
 //   kCluster = false: one CTA per SM, records in global memory (L2), a
 //                     monotonic-counter grid barrier per step.
 #include <climits>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -37,14 +38,14 @@ namespace cg = cooperative_groups;
 
 namespace idk {
 
-struct CpqrRec {
-    double vmax;    // largest live norm among this CTA's candidates (-1: none)
-    long long pos;  // lowest qualifying position (LLONG_MAX: none)
-    long long col;  // its column id
-    double tau;     // the candidate's reflector, built before the exchange
-    double beta;    //   (qr.cpp:16-28 on its active rows)
-    double scale;
-};
+// Exchange slot of one CTA for one exchange: a 4-double header (candidate
+// column id, its next reflector tau/beta/scale) followed by the candidate's
+// active rows.  Records: grid mode uses LL-style tagged 64-bit words
+// (payload32 << 32 | tag32; aligned 64-bit stores are single-copy atomic), so
+// polling the G records is the barrier; cluster mode keeps records in shared
+// memory behind barrier.cluster.
+constexpr int kHdr = 4;
+constexpr int kRecWords = 4;  // vmax hi | vmax lo | pos | pad
 
 struct ResidentArgs {
     double* W;
@@ -58,18 +59,16 @@ struct ResidentArgs {
     long long* pos_out;
     long long* pivots;
     double* taus;
-    // grid-exchange buffers (global); unused in cluster mode
-    CpqrRec* rec;     // [2][G]
-    double* colbuf;   // [2][G][m]
-    CpqrRec* rec2;    // [G]
-    double* colbuf2;  // [G][m]
-    unsigned* barrier;
-    long long* trace;  // optional: %globaltimer at 8 phase marks per step, every CTA
+    // grid-exchange buffers (global, zeroed before launch); unused in cluster mode
+    unsigned long long* rec;  // [3][G][kRecWords]
+    double* slots;            // [3][G][kHdr + m]
+    unsigned* barrier;        // debug: optional grid barrier before each exchange
+    long long* trace;         // optional: %globaltimer at 8 phase marks per step, every CTA
 };
 
 namespace {
 
-constexpr double kRecomp = 1e-6;      // qr.cpp:100
+constexpr double kRecomp = 1e-6;  // qr.cpp:100
 
 template <int S>
 __device__ __forceinline__ unsigned group_mask() {
@@ -98,26 +97,6 @@ __device__ __forceinline__ long long globaltimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
-}
-
-__device__ __forceinline__ void st_rec_cg(CpqrRec* p, const CpqrRec& r) {
-    double2* d = reinterpret_cast<double2*>(p);
-    __stcg(d, make_double2(r.vmax, __longlong_as_double(r.pos)));
-    __stcg(d + 1, make_double2(__longlong_as_double(r.col), r.tau));
-    __stcg(d + 2, make_double2(r.beta, r.scale));
-}
-
-__device__ __forceinline__ CpqrRec ld_rec_cg(const CpqrRec* p) {
-    const double2* d = reinterpret_cast<const double2*>(p);
-    const double2 a = __ldcg(d), b = __ldcg(d + 1), c = __ldcg(d + 2);
-    CpqrRec r;
-    r.vmax = a.x;
-    r.pos = __double_as_longlong(a.y);
-    r.col = __double_as_longlong(b.x);
-    r.tau = b.y;
-    r.beta = c.x;
-    r.scale = c.y;
-    return r;
 }
 
 // sqrt(v) >= (1 - 1e-14) * sqrt(vmax) (qr.cpp:71-73) evaluated exactly, with
@@ -151,6 +130,21 @@ __device__ __forceinline__ void reflector(double alpha, double tail, int len, do
     }
 }
 
+__device__ __forceinline__ unsigned long long tagged(unsigned payload, unsigned tag) {
+    return (static_cast<unsigned long long>(payload) << 32) | tag;
+}
+
+// Strong (relaxed, gpu scope) 16-byte accesses for the tagged records: each
+// 64-bit element is single-copy atomic and takes part in the memory model.
+__device__ __forceinline__ void st_relaxed_v2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ void ld_relaxed_v2(const unsigned long long* p, unsigned long long& a,
+                                              unsigned long long& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
 }  // namespace
 
 #define IDK_REP32(M) \
@@ -170,21 +164,20 @@ cpqr_resident_kernel(ResidentArgs a) {
     const int m = a.m, nc = a.nc, l0 = a.l0, lds = a.lds;
     const int span = max(m, l0 + R * S);
     const int xlen = ((kGuard + span + S + 1) + 1) & ~1;
+    const int slot_len = kHdr + ((m + 1) & ~1);
     double* xbuf = sm;
     double* xv = xbuf + kGuard;
-    double* rows = xbuf + xlen;                               // nc * lds
-    double* s_live = rows + static_cast<size_t>(nc) * lds;    // nc
-    double* s_anchor = s_live + nc;                           // nc
+    double* rows = xbuf + xlen;                                      // nc * lds
+    double* s_live = rows + static_cast<size_t>(nc) * lds;           // nc
+    double* s_anchor = s_live + nc;                                  // nc
     long long* s_pos = reinterpret_cast<long long*>(s_anchor + nc);  // nc (positions < 2^31)
-    const int mpad = (m + 1) & ~1;
-    double* ccol = reinterpret_cast<double*>(s_pos + nc);     // cluster: [2][mpad] + [mpad]
+    double* cslots = reinterpret_cast<double*>(s_pos + nc);          // cluster: [3][slot_len]
 
     __shared__ double red_d[32];
     __shared__ long long red_l[32];
     __shared__ double s_sc[3];      // tau, beta, scale of the current pivot
-    __shared__ long long s_sel[3];  // pivot column, its position before the swap, winning CTA
-    __shared__ double s_cand[3];    // candidate reflector: tau, beta, scale
-    __shared__ CpqrRec s_rec[3];    // cluster: own records [2] + tie pass
+    __shared__ long long s_sel[3];  // pivot column, its position before the swap, winning CTA (-2: tie pass)
+    __shared__ double s_rec[3][2];  // cluster: own records {vmax, pos}
 
     const int tid = threadIdx.x, T = blockDim.x;
     const int lane = tid & 31, wid = tid >> 5, nw = T >> 5;
@@ -199,21 +192,9 @@ cpqr_resident_kernel(ResidentArgs a) {
     const int nsr = l0 / S;  // l0 is a multiple of S
     double* myrows = rows + static_cast<size_t>(lc < nc ? lc : 0) * lds;
     const int gbase = lane & ~(S - 1);
-    unsigned epoch = 0;
-    // This thread's share of its column's next-reflector inputs: alpha = the
-    // entry at the next step's row, tail = sum of squares below it.
-    double p_alpha = 0.0, p_tail = 0.0;
 
     auto trace = [&](int s, int ph) {
         if (a.trace != nullptr && tid == 0) a.trace[(static_cast<size_t>(me) * (a.k + 1) + s) * 8 + ph] = globaltimer();
-    };
-
-    auto barrier_all = [&]() {
-        if constexpr (kCluster) {
-            cg::this_cluster().sync();
-        } else {
-            grid_barrier(a.barrier, epoch);
-        }
     };
 
     for (int i = tid; i < xlen; i += T) xbuf[i] = 0.0;
@@ -226,16 +207,12 @@ cpqr_resident_kernel(ResidentArgs a) {
         const int i = l0 + q + S * r;
         yr[r] = (active && i < m) ? W[col * a.ldw + i] : 0.0;
         part = fma(yr[r], yr[r], part);
-        if (i == 0) p_alpha = yr[r];
-        else p_tail = fma(yr[r], yr[r], p_tail);
     }
     for (int r = 0; r < nsr; ++r) {
         const int i = q + S * r;
         const double v = active ? W[col * a.ldw + i] : 0.0;
         if (lc < nc) myrows[i] = v;
         part = fma(v, v, part);
-        if (i == 0) p_alpha = v;
-        else p_tail = fma(v, v, p_tail);
     }
     part = group_sum<S>(part);
     if (active && q == 0) {
@@ -244,10 +221,31 @@ cpqr_resident_kernel(ResidentArgs a) {
         s_pos[lc] = col;
     }
 
+    // This group's column: alpha = row `first`, tail = sum of squares below it.
+    auto partials = [&](int first, double& al, double& tl) {
+        double a0 = 0.0, t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = l0 + q + S * r;
+            if (i == first) a0 = yr[r];
+            else if (i > first) {
+                if (r & 1) t1 = fma(yr[r], yr[r], t1);
+                else t0 = fma(yr[r], yr[r], t0);
+            }
+        }
+        for (int r = first / S; r < nsr; ++r) {
+            const int i = q + S * r;
+            const double v = myrows[i];
+            if (i == first) a0 = v;
+            else if (i > first) t0 = fma(v, v, t0);
+        }
+        al = group_sum<S>(a0);
+        tl = group_sum<S>(t0 + t1);
+    };
+
     // CTA argmax (qr.cpp:66-78 over this CTA's columns): the max live norm,
     // then the lowest position that qualifies against it; 32-bit redux.sync
-    // per warp and one __syncthreads per pass.  Returns the position
-    // (INT_MAX: none); the group whose position matches is the candidate.
+    // per warp and one __syncthreads per pass.
     auto local_max = [&](bool cand, double lv) -> double {
         const double mx = warp_max_nonneg(cand ? lv : -1.0);
         if (lane == 0) red_d[wid] = mx;
@@ -267,109 +265,114 @@ cpqr_resident_kernel(ResidentArgs a) {
         return best == 0xffffffffu ? INT_MAX : static_cast<int>(best);
     };
 
-    // Candidate column (local index winlc) -> exchange slot rows first..m-1:
-    // its group stores the register rows and turns its (alpha, tail) partials
-    // into the next reflector (qr.cpp:16-28); every thread copies a share of
-    // its shared-memory rows.
-    auto push_candidate = [&](int winlc, int first, double* dst, double pa, double pt) {
-        if (winlc >= nc) return;
-        if (lc == winlc) {
+    auto slot_ptr = [&](int slot, int g) -> double* {
+        if constexpr (kCluster) {
+            double* mineptr = cslots + slot * slot_len;
+            return g == me ? mineptr : cg::this_cluster().map_shared_rank(mineptr, g);
+        } else {
+            return a.slots + (static_cast<size_t>(slot) * G + g) * slot_len;
+        }
+    };
+
+    // Publish this CTA's candidate (local index winlc, position winpos) for the
+    // exchange `tag` in `slot`: header + rows first..m-1, then the record.
+    auto publish = [&](int slot, unsigned tag, double mx, int winpos, int winlc, int first) {
+        const bool have = winpos != INT_MAX;
+        double* dst = slot_ptr(slot, me);
+        if (have && lc == winlc) {
+            double al, tl;
+            partials(first, al, tl);
+            double tau, beta, scale;
+            reflector(al, tl, m - first, tau, beta, scale);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int i = l0 + q + S * r;
-                if (i >= first && i < m) dst[i - first] = yr[r];
+                if (i >= first && i < m) dst[kHdr + i - first] = yr[r];
             }
-            const double al = group_sum<S>(pa);
-            const double tl = group_sum<S>(pt);
             if (q == 0) {
-                double tau, beta, scale;
-                reflector(al, tl, m - first, tau, beta, scale);
-                s_cand[0] = tau;
-                s_cand[1] = beta;
-                s_cand[2] = scale;
-                red_l[31] = c0 + winlc;
+                dst[0] = __longlong_as_double(c0 + winlc);
+                dst[1] = tau;
+                dst[2] = beta;
+                dst[3] = scale;
             }
         }
-        const double* cr = rows + static_cast<size_t>(winlc) * lds;
-        for (int i = first + tid; i < l0; i += T) dst[i - first] = cr[i];
-    };
-
-    auto write_record = [&](int slot, double mx, int winpos) {
-        const bool have = winpos != INT_MAX;
-        CpqrRec rc;
-        rc.vmax = mx;
-        rc.pos = have ? winpos : LLONG_MAX;
-        rc.col = have ? red_l[31] : -1;
-        rc.tau = have ? s_cand[0] : 0.0;
-        rc.beta = have ? s_cand[1] : 0.0;
-        rc.scale = have ? s_cand[2] : 1.0;
-        if constexpr (kCluster) {
-            s_rec[slot] = rc;
-        } else {
-            st_rec_cg(slot == 2 ? a.rec2 + me : a.rec + static_cast<size_t>(slot) * G + me, rc);
+        if (have) {  // shared-memory rows of the candidate, copied by everyone
+            const double* cr = rows + static_cast<size_t>(winlc) * lds;
+            for (int i = first + tid; i < l0; i += T) dst[kHdr + i - first] = cr[i];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
+            if constexpr (kCluster) {
+                s_rec[slot][0] = mx;
+                s_rec[slot][1] = __longlong_as_double(static_cast<long long>(pos32));
+            } else {
+                __threadfence();  // slot data before the tagged record (release)
+                const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
+                unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * kRecWords;
+                st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
+                st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
+            }
         }
     };
 
-    auto rec_of = [&](int slot, int g) -> CpqrRec {
+    // Record of CTA g for exchange `tag`: {vmax, pos}; grid mode spins until
+    // all three words carry the tag.
+    auto read_rec = [&](int slot, int g, unsigned tag, double& vmax, unsigned& pos) {
         if constexpr (kCluster) {
-            return *cg::this_cluster().map_shared_rank(&s_rec[slot], g);
+            const double* rp = cg::this_cluster().map_shared_rank(&s_rec[slot][0], g);
+            vmax = rp[0];
+            pos = static_cast<unsigned>(__double_as_longlong(rp[1]));
         } else {
-            return ld_rec_cg(slot == 2 ? a.rec2 + g : a.rec + static_cast<size_t>(slot) * G + g);
+            const unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + g) * kRecWords;
+            unsigned long long x0, x1, x2, x3;
+            for (;;) {
+                ld_relaxed_v2(rp, x0, x1);
+                ld_relaxed_v2(rp + 2, x2, x3);
+                if (static_cast<unsigned>(x0) == tag && static_cast<unsigned>(x1) == tag &&
+                    static_cast<unsigned>(x2) == tag)
+                    break;
+            }
+            vmax = __longlong_as_double(static_cast<long long>(((x0 >> 32) << 32) | (x1 >> 32)));
+            pos = static_cast<unsigned>(x2 >> 32);
         }
     };
 
-    auto col_of = [&](int slot, int g) -> const double* {
-        if constexpr (kCluster) {
-            return cg::this_cluster().map_shared_rank(ccol + slot * mpad, g);
-        } else {
-            return slot == 2 ? a.colbuf2 + static_cast<size_t>(g) * m : a.colbuf + (static_cast<size_t>(slot) * G + g) * m;
-        }
-    };
-
-    auto cand_slot = [&](int slot) -> double* {
-        return kCluster ? (ccol + slot * mpad) : (slot == 2 ? a.colbuf2 + static_cast<size_t>(me) * m
-                                                            : a.colbuf + (static_cast<size_t>(slot) * G + me) * m);
-    };
-
-    // After the barrier warp 0 alone reduces the G records (identical in
-    // every CTA) and posts the winner; then all threads copy its column into
-    // xv, already scaled by the winner's reflector.
     constexpr int kRecPerLane = kCluster ? 1 : 5;  // G <= 32 (cluster) or <= 160 (grid)
-    auto post_winner = [&](const CpqrRec& w, long long wpos, int wg, bool amb) {
-        s_sel[0] = amb ? -2 : w.col;
-        s_sel[1] = wpos;
-        s_sel[2] = wg;
-        s_sc[0] = w.tau;
-        s_sc[1] = w.beta;
-        s_sc[2] = w.scale;
-    };
-    auto select = [&](int first, int parity) {
+
+    // Wait for every CTA's record of exchange `tag`, reduce them (identical in
+    // every CTA), then copy the winner's column -- scaled by its reflector --
+    // into xv.  `first` = the step the new pivot is for.
+    unsigned epoch = 0;
+    auto exchange = [&](int parity, unsigned tag, int first) {
+        if constexpr (kCluster) cg::this_cluster().sync();
+        if constexpr (!kCluster) {
+            if (a.barrier != nullptr) grid_barrier(a.barrier, epoch);
+        }
         int slot = parity;
         if (wid == 0) {
-            CpqrRec r[kRecPerLane];
+            double v[kRecPerLane];
+            unsigned p[kRecPerLane];
 #pragma unroll
             for (int t = 0; t < kRecPerLane; ++t) {
                 const int g = lane + 32 * t;
-                if (g < G) {
-                    r[t] = rec_of(parity, g);
-                } else {
-                    r[t].vmax = -1.0;
-                    r[t].pos = LLONG_MAX;
-                }
+                v[t] = -1.0;
+                p[t] = 0xffffffffu;
+                if (g < G) read_rec(parity, g, tag, v[t], p[t]);
             }
+            if constexpr (!kCluster) __threadfence();  // acquire: slot data after the records
             double vmax = -1.0;
 #pragma unroll
-            for (int t = 0; t < kRecPerLane; ++t) vmax = fmax(vmax, r[t].vmax);
-            if (first > 0) trace(first - 1, 4);
+            for (int t = 0; t < kRecPerLane; ++t) vmax = fmax(vmax, v[t]);
             vmax = warp_max_nonneg(vmax);
             unsigned best = 0xffffffffu;
             int bt = 0, amb = 0;
 #pragma unroll
             for (int t = 0; t < kRecPerLane; ++t) {
-                if (r[t].vmax >= 0.0 && qualifies(r[t].vmax, vmax)) {
-                    amb |= r[t].vmax != vmax;
-                    if (static_cast<unsigned>(r[t].pos) < best) {
-                        best = static_cast<unsigned>(r[t].pos);
+                if (v[t] >= 0.0 && qualifies(v[t], vmax)) {
+                    amb |= v[t] != vmax;
+                    if (p[t] < best) {
+                        best = p[t];
                         bt = t;
                     }
                 }
@@ -377,69 +380,75 @@ cpqr_resident_kernel(ResidentArgs a) {
             amb = __any_sync(0xffffffffu, amb);
             const unsigned wb = __reduce_min_sync(0xffffffffu, best);
             if (best == wb && best != 0xffffffffu) {  // unique lane: positions are distinct
-                CpqrRec w = r[0];
-#pragma unroll
-                for (int t = 1; t < kRecPerLane; ++t)
-                    if (bt == t) w = r[t];
-                post_winner(w, wb, lane + 32 * bt, amb != 0);
+                s_sel[0] = amb ? -2 : 0;
+                s_sel[1] = wb;
+                s_sel[2] = lane + 32 * bt;
             }
             if (lane == 0) red_d[0] = vmax;
         }
         __syncthreads();
-        if (first > 0) trace(first - 1, 7);
         if (s_sel[0] == -2) {
             // Exact tie pass: lowest position with sqrt(live) >= the global threshold.
             const double vmax = red_d[0];
             const bool cand = active && q == 0 && s_pos[lc] >= first;
             int winlc;
             const int winpos = local_pick(cand, cand ? s_live[lc] : -1.0, cand ? s_pos[lc] : 0, vmax, winlc);
-            push_candidate(winpos == INT_MAX ? nc : winlc, first, cand_slot(2), p_alpha, p_tail);
-            __syncthreads();
-            if (tid == 0) write_record(2, 0.0, winpos);
-            barrier_all();
+            publish(2, tag, 0.0, winpos, winlc, first);
+            if constexpr (kCluster) cg::this_cluster().sync();
             slot = 2;
             if (wid == 0) {
                 unsigned b2 = 0xffffffffu;
-                CpqrRec r2;
                 int g2 = -1;
                 for (int g = lane; g < G; g += 32) {
-                    const CpqrRec rr = rec_of(2, g);
-                    if (static_cast<unsigned>(rr.pos) < b2) {
-                        b2 = static_cast<unsigned>(rr.pos);
-                        r2 = rr;
+                    double vv;
+                    unsigned pp;
+                    read_rec(2, g, tag, vv, pp);
+                    if (pp < b2) {
+                        b2 = pp;
                         g2 = g;
                     }
                 }
+                if constexpr (!kCluster) __threadfence();
                 const unsigned wb = __reduce_min_sync(0xffffffffu, b2);
-                if (b2 == wb && b2 != 0xffffffffu) post_winner(r2, wb, g2, false);
+                if (b2 == wb && b2 != 0xffffffffu) {
+                    s_sel[0] = 0;
+                    s_sel[1] = wb;
+                    s_sel[2] = g2;
+                }
             }
             __syncthreads();
         }
-        {
-            const int len = m - first;
-            const double tau = s_sc[0], scale = s_sc[2];
-            const double* src = col_of(slot, static_cast<int>(s_sel[2]));
-            for (int i = tid; i < len; i += T) {
-                const double x = kCluster ? src[i] : __ldcg(src + i);
-                xv[i] = tau != 0.0 ? (i == 0 ? 1.0 : mul_rn(x, scale)) : x;
-            }
-            for (int i = len + tid; i < span + S; i += T) xv[i] = 0.0;  // stale tail of the previous pivot
+        // All threads: header + winner's column (one round trip), scaled into xv.
+        const double* src = slot_ptr(slot, static_cast<int>(s_sel[2]));
+        const int len = m - first;
+        const double h0 = kCluster ? src[0] : __ldcg(src);
+        const double tau = kCluster ? src[1] : __ldcg(src + 1);
+        const double beta = kCluster ? src[2] : __ldcg(src + 2);
+        const double scale = kCluster ? src[3] : __ldcg(src + 3);
+        for (int i = tid; i < len; i += T) {
+            const double x = kCluster ? src[kHdr + i] : __ldcg(src + kHdr + i);
+            xv[i] = tau != 0.0 ? (i == 0 ? 1.0 : mul_rn(x, scale)) : x;
+        }
+        for (int i = len + tid; i < span + S; i += T) xv[i] = 0.0;  // stale tail of the previous pivot
+        if (tid == 0) {
+            s_sel[0] = __double_as_longlong(h0);
+            s_sc[0] = tau;
+            s_sc[1] = beta;
+            s_sc[2] = scale;
         }
         __syncthreads();
     };
 
     // ---- pivot 0 ----
     {
+        __syncthreads();
         const bool cand = active && q == 0;
         const double lv = cand ? s_live[lc] : -1.0;
         const double mx = local_max(cand, lv);
         int winlc;
         const int winpos = local_pick(cand, lv, cand ? s_pos[lc] : 0, mx, winlc);
-        push_candidate(winpos == INT_MAX ? nc : winlc, 0, cand_slot(0), p_alpha, p_tail);
-        __syncthreads();
-        if (tid == 0) write_record(0, mx, winpos);
-        barrier_all();
-        select(0, 0);
+        publish(0, 1u, mx, winpos, winlc, 0);
+        exchange(0, 1u, 0);
     }
 
     for (int s = 0; s < a.k; ++s) {
@@ -465,12 +474,6 @@ cpqr_resident_kernel(ResidentArgs a) {
         const int rr0 = dreg <= 0 ? 0 : dreg / S;
         const int sr0 = s / S;
         const double* xr = xv + (l0 + q - s);  // xr[S*r] = v for register row r
-        p_alpha = 0.0;
-        p_tail = 0.0;
-        auto tpart = [&](int i, double v) {
-            if (i == s + 1) p_alpha = v;
-            else if (i > s + 1) p_tail = fma(v, v, p_tail);
-        };
         bool cand = false;
         double lv = -1.0;
         if (active && col == piv) {
@@ -544,21 +547,14 @@ cpqr_resident_kernel(ResidentArgs a) {
                     const int i = q + S * r;
                     const double y0 = myrows[i], y1 = myrows[i + S], y2 = myrows[i + 2 * S], y3 = myrows[i + 3 * S];
                     const double v0 = xv[i - s], v1 = xv[i - s + S], v2 = xv[i - s + 2 * S], v3 = xv[i - s + 3 * S];
-                    const double n0 = fma(-w, v0, y0), n1 = fma(-w, v1, y1), n2 = fma(-w, v2, y2), n3 = fma(-w, v3, y3);
-                    myrows[i] = n0;
-                    myrows[i + S] = n1;
-                    myrows[i + 2 * S] = n2;
-                    myrows[i + 3 * S] = n3;
-                    tpart(i, n0);
-                    tpart(i + S, n1);
-                    tpart(i + 2 * S, n2);
-                    tpart(i + 3 * S, n3);
+                    myrows[i] = fma(-w, v0, y0);
+                    myrows[i + S] = fma(-w, v1, y1);
+                    myrows[i + 2 * S] = fma(-w, v2, y2);
+                    myrows[i + 3 * S] = fma(-w, v3, y3);
                 }
                 for (; r < nsr; ++r) {
                     const int i = q + S * r;
-                    const double nv = fma(-w, xv[i - s], myrows[i]);
-                    myrows[i] = nv;
-                    tpart(i, nv);
+                    myrows[i] = fma(-w, xv[i - s], myrows[i]);
                 }
                 switch (rr0) {
 #define IDK_AXPY_CASE(r)                                         \
@@ -571,16 +567,14 @@ cpqr_resident_kernel(ResidentArgs a) {
                         break;
                 }
                 head = ys - w;  // row s has v_0 = 1
-            } else {
-                for (int r = sr0; r < nsr; ++r) tpart(q + S * r, myrows[q + S * r]);
             }
-#pragma unroll
-            for (int r = 0; r < R; ++r) tpart(l0 + q + S * r, yr[r]);  // rows >= m hold zeros
             lv = sub_rn(s_live[lc], mul_rn(head, head));
             if (lv < 0.0) lv = 0.0;
             if (lv <= mul_rn(kRecomp, s_anchor[lc])) {
-                // fresh = sum_{i > s} y_i^2 (qr.cpp:101-104) = alpha^2 + tail of the next step
-                lv = group_sum<S>(fma(p_alpha, p_alpha, p_tail));
+                // fresh = sum_{i > s} y_i^2 (qr.cpp:101-104)
+                double al, tl;
+                partials(s + 1, al, tl);
+                lv = fma(al, al, tl);
                 if (q == 0) s_anchor[lc] = lv;
             }
             if (q == 0) s_live[lc] = lv;
@@ -595,13 +589,9 @@ cpqr_resident_kernel(ResidentArgs a) {
         int winlc;
         const int winpos = local_pick(cand, lv, mypos, mx, winlc);
         trace(s, 2);
-        push_candidate(winpos == INT_MAX ? nc : winlc, s + 1, cand_slot(parity), p_alpha, p_tail);
-        __syncthreads();
-        if (tid == 0) write_record(parity, mx, winpos);
+        publish(parity, static_cast<unsigned>(s + 2), mx, winpos, winlc, s + 1);
         trace(s, 3);
-        barrier_all();
-        trace(s, 5);
-        select(s + 1, parity);
+        exchange(parity, static_cast<unsigned>(s + 2), s + 1);
         trace(s, 6);
     }
 
@@ -637,11 +627,11 @@ int pad_lds(int l0, int S) {
 }
 
 size_t resident_smem(int m, int nc, int l0, int lds, int S, int R, bool cluster) {
-    const size_t mpad = static_cast<size_t>((m + 1) & ~1);
+    const size_t slot_len = kHdr + static_cast<size_t>((m + 1) & ~1);
     const int span = std::max(m, l0 + R * S);
     const size_t xlen = static_cast<size_t>(((kGuard + span + S + 1) + 1) & ~1);
     size_t d = xlen + static_cast<size_t>(nc) * lds + 2 * static_cast<size_t>(nc) + static_cast<size_t>(nc);
-    if (cluster) d += 3 * mpad;
+    if (cluster) d += 3 * slot_len;
     return d * sizeof(double);
 }
 
@@ -740,7 +730,8 @@ void cpqr_resident_set_trace(long long* p) { g_trace = p; }
 size_t cpqr_resident_exchange_bytes(const ResidentPlan& p, int m) {
     if (!p.ok || p.cluster) return 0;
     const size_t G = static_cast<size_t>(p.G);
-    return sizeof(CpqrRec) * 3 * G + sizeof(double) * 3 * G * static_cast<size_t>(m) + 256;
+    const size_t slot_len = kHdr + static_cast<size_t>((m + 1) & ~1);
+    return sizeof(unsigned long long) * kRecWords * 3 * G + sizeof(double) * 3 * G * slot_len + 256;
 }
 
 cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, int m, int64_t n, int k,
@@ -760,11 +751,8 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     a.taus = taus;
     const size_t G = static_cast<size_t>(p.G);
     char* e = static_cast<char*>(exch);
-    a.rec = reinterpret_cast<CpqrRec*>(e);
-    a.rec2 = a.rec + 2 * G;
-    a.colbuf = reinterpret_cast<double*>(e + sizeof(CpqrRec) * 3 * G);
-    a.colbuf2 = a.colbuf + 2 * G * static_cast<size_t>(m);
-    a.barrier = barrier;
+    a.rec = reinterpret_cast<unsigned long long*>(e);
+    a.slots = reinterpret_cast<double*>(e + sizeof(unsigned long long) * kRecWords * 3 * G);
     a.trace = g_trace;
     void* args[] = {&a};
     if (p.cluster) {
@@ -791,8 +779,15 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     if (!fn) return cudaErrorInvalidValue;
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
     if (err != cudaSuccess) return err;
-    err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream);
+    // records start untagged (tags are 1..k, so stale records never match)
+    err = cudaMemsetAsync(exch, 0, sizeof(unsigned long long) * kRecWords * 3 * G, stream);
     if (err != cudaSuccess) return err;
+    a.barrier = nullptr;
+    if (getenv("IDK_DEBUG_GRID_BARRIER")) {
+        a.barrier = barrier;
+        err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream);
+        if (err != cudaSuccess) return err;
+    }
     return cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(p.threads), args, p.smem, stream);
 }
 
