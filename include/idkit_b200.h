@@ -178,6 +178,16 @@ IDK_API int idk_select_columns(idk_handle h, const double* d_a, int64_t m, int64
 IDK_API int idk_id_auto_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int method, uint64_t seed,
                      int64_t p, int omega_mode, int64_t* h_cols, double* h_z, double* h_c, int* transposed);
 
+/* Pipelined host entry: `count` independent IDs of m x n matrices h_a[i]
+ * (host, ld = m), results into h_cols[i], h_z[i] (k * max(m, n)) and, if
+ * h_c != NULL, h_c[i].  The upload of matrix i+1 and the download of result
+ * i-1 overlap the compute of ID i on separate streams (pinned host buffers
+ * make the copies asynchronous); statuses are checked once at the end, the
+ * first failure is reported with its index. */
+IDK_API int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a, int64_t m, int64_t n,
+                                  int64_t k, int method, uint64_t seed, int64_t p, int omega_mode,
+                                  int64_t* const* h_cols, double* const* h_z, double* const* h_c, int* transposed);
+
 #ifdef __cplusplus
 }
 #endif

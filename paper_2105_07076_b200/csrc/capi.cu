@@ -37,6 +37,12 @@ struct idk_context {
     int64_t launches = 0;
     int cpqr_mode = IDK_CPQR_AUTO;
     bool batched_exact = false;
+    // pipelined host entry: status words land here (pinned) instead of a sync per ID
+    int* async_status = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out[2] = {};
+    int* h_status_many = nullptr;
+    int64_t h_status_many_cap = 0;
     // per-stage CUDA events on the launching stream (idk_set_profiling)
     bool profiling = false;
     cudaEvent_t ev[6] = {};
@@ -198,6 +204,10 @@ int factor_and_solve(idk_context* h, const CpqrChoice& ch, double* W, int64_t mr
     }
     mark(h, 5);
     IDK_CUDA(cudaMemcpyAsync(d_cols, piv, sizeof(long long) * k, cudaMemcpyDeviceToDevice, h->stream));
+    if (h->async_status) {  // pipelined entry: the caller checks the status word later
+        IDK_CUDA(cudaMemcpyAsync(h->async_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        return IDK_OK;
+    }
     IDK_CUDA(cudaMemcpyAsync(h->h_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     IDK_CUDA(cudaStreamSynchronize(h->stream));
     collect_stage_times(h);
@@ -368,8 +378,16 @@ int idk_destroy(idk_handle h) {
     if (h->io) cudaFree(h->io);
     if (h->h_status) cudaFreeHost(h->h_status);
     if (h->h_omega) cudaFreeHost(h->h_omega);
+    if (h->h_status_many) cudaFreeHost(h->h_status_many);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+        if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
+        if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
+        if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
+    }
+    if (h->s_in) cudaStreamDestroy(h->s_in);
+    if (h->s_out) cudaStreamDestroy(h->s_out);
     delete h;
     return IDK_OK;
 }
@@ -597,6 +615,90 @@ int idk_id_from_sketch(idk_handle h, double* d_y, int64_t l, int64_t n, int64_t 
     IDK_CUDA(cudaStreamSynchronize(h->stream));
     if (*h->h_status != 0x7f7f7f7f)
         return set_err(h, IDK_ERR_SINGULAR, "solve_triangular: zero diagonal at index " + std::to_string(*h->h_status));
+    return IDK_OK;
+}
+
+int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a, int64_t m, int64_t n, int64_t k,
+                          int method, uint64_t seed, int64_t p, int omega_mode, int64_t* const* h_cols,
+                          double* const* h_z, double* const* h_c, int* transposed) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (count < 0 || (count > 0 && (!h_a || !h_cols || !h_z)))
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_auto_host_many: bad arguments");
+    int rc = check_k(h, m, n, k, "id_auto");
+    if (rc) return rc;
+    if (omega_mode == IDK_OMEGA_VERBATIM)
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_auto_host_many: verbatim omega needs the device entry");
+    if (count == 0) return IDK_OK;
+    const bool tall = m > n;
+    const int64_t zc = tall ? m : n, crow = tall ? n : m;
+    const bool want_c = h_c != nullptr;
+    // two buffer sets: ID i+1's upload overlaps ID i's compute and ID i-1's download
+    Carve cv;
+    size_t aofs[2], cofs[2], zofs[2], ccofs[2];
+    for (int b = 0; b < 2; ++b) {
+        aofs[b] = cv.take(sizeof(double) * m * n);
+        cofs[b] = cv.take(sizeof(int64_t) * k);
+        zofs[b] = cv.take(sizeof(double) * k * zc);
+        ccofs[b] = cv.take(sizeof(double) * crow * k);
+    }
+    if ((rc = ensure(h, &h->io, &h->io_cap, cv.total))) return rc;
+    if (!h->s_in) {
+        IDK_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+        IDK_CUDA(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            IDK_CUDA(cudaEventCreateWithFlags(&h->ev_in[b], cudaEventDisableTiming));
+            IDK_CUDA(cudaEventCreateWithFlags(&h->ev_done[b], cudaEventDisableTiming));
+            IDK_CUDA(cudaEventCreateWithFlags(&h->ev_out[b], cudaEventDisableTiming));
+        }
+    }
+    if (count > h->h_status_many_cap) {
+        if (h->h_status_many) cudaFreeHost(h->h_status_many);
+        h->h_status_many = nullptr;
+        h->h_status_many_cap = 0;
+        IDK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->h_status_many), sizeof(int) * count));
+        h->h_status_many_cap = count;
+    }
+    const bool prof = h->profiling;
+    h->profiling = false;
+    for (int64_t i = 0; i < count; ++i) {
+        const int b = static_cast<int>(i & 1);
+        double* d_a = reinterpret_cast<double*>(h->io + aofs[b]);
+        int64_t* d_cols = reinterpret_cast<int64_t*>(h->io + cofs[b]);
+        double* d_z = reinterpret_cast<double*>(h->io + zofs[b]);
+        double* d_c = want_c ? reinterpret_cast<double*>(h->io + ccofs[b]) : nullptr;
+        if (i >= 2) IDK_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_out[b], 0));  // set b fully drained
+        IDK_CUDA(cudaMemcpyAsync(d_a, h_a[i], sizeof(double) * m * n, cudaMemcpyHostToDevice, h->s_in));
+        IDK_CUDA(cudaEventRecord(h->ev_in[b], h->s_in));
+        IDK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
+        h->h_status_many[i] = 0x7f7f7f7f;
+        h->async_status = h->h_status_many + i;
+        rc = id_auto_dev(h, d_a, m, n, m, k, method, seed, p, omega_mode, nullptr, d_cols, d_z, d_c, transposed);
+        h->async_status = nullptr;
+        if (rc) {
+            h->profiling = prof;
+            cudaStreamSynchronize(h->stream);
+            return rc;
+        }
+        IDK_CUDA(cudaEventRecord(h->ev_done[b], h->stream));
+        IDK_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_done[b], 0));
+        IDK_CUDA(cudaMemcpyAsync(h_cols[i], d_cols, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->s_out));
+        IDK_CUDA(cudaMemcpyAsync(h_z[i], d_z, sizeof(double) * k * zc, cudaMemcpyDeviceToHost, h->s_out));
+        if (want_c) IDK_CUDA(cudaMemcpyAsync(h_c[i], d_c, sizeof(double) * crow * k, cudaMemcpyDeviceToHost, h->s_out));
+        IDK_CUDA(cudaEventRecord(h->ev_out[b], h->s_out));
+    }
+    h->profiling = prof;
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->s_out));
+    for (int64_t i = 0; i < count; ++i) {
+        const int bad = h->h_status_many[i];
+        if (bad != 0x7f7f7f7f) {
+            const bool det = method == 0;
+            return set_err(h, det ? IDK_ERR_NOT_POSDEF : IDK_ERR_SINGULAR,
+                           "id_auto_host_many: matrix " + std::to_string(i) + ": R11 diagonal " +
+                               std::to_string(bad) + " is zero");
+        }
+    }
     return IDK_OK;
 }
 

@@ -258,6 +258,38 @@ def id_auto(a, k: int, method: int = DETERMINISTIC, seed: int = 0, p: int = 0,
     return IdResult(cols, z, c, bool(tr.value))
 
 
+def id_auto_many(mats, k: int, method: int = DETERMINISTIC, seed: int = 0, p: int = 0,
+                 omega_mode: int = OMEGA_PHILOX, want_c: bool = True, out=None):
+    """Pipelined host entry: IDs of several host matrices (same shape); uploads,
+    compute and downloads overlap on separate streams.  Pass pinned, column-major
+    numpy arrays for asynchronous copies.  `out` (optional) = preallocated
+    (cols, z, c) lists to write into.  Returns (cols list, z list, c list, transposed)."""
+    mats = [np.asfortranarray(x, dtype=np.float64) for x in mats]
+    cnt = len(mats)
+    m, n = mats[0].shape
+    if any(x.shape != (m, n) for x in mats):
+        raise InvalidArgument("id_auto_many: all matrices must have the same shape")
+    tall = m > n
+    zc, crow = (m, n) if tall else (n, m)
+    if out is None:
+        cols = [np.empty(k, dtype=np.int64) for _ in range(cnt)]
+        zs = [np.empty((k, zc), order="F") for _ in range(cnt)]
+        cs = [np.empty((crow, k), order="F") for _ in range(cnt)] if want_c else None
+    else:
+        cols, zs, cs = out
+    P = C.c_void_p * max(cnt, 1)
+    pa = P(*[x.ctypes.data for x in mats])
+    pcol = P(*[x.ctypes.data for x in cols])
+    pz = P(*[x.ctypes.data for x in zs])
+    pc = P(*[x.ctypes.data for x in cs]) if cs is not None else None
+    ctx = context(0)
+    ctx.bind_stream()
+    tr = C.c_int(0)
+    ctx.check(ctx.lib.idk_id_auto_host_many(ctx.h, cnt, pa, m, n, k, method, seed, p, omega_mode, pcol, pz, pc,
+                                            C.byref(tr)))
+    return cols, zs, cs, bool(tr.value)
+
+
 def optim_id_batched(a, k: int, want_c: bool = True):
     """BASELINE cfg3: `a` is a (batch, n, m) contiguous CUDA tensor holding
     batch column-major m x n matrices (i.e. a[b].t() is matrix b).

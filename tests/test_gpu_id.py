@@ -299,3 +299,29 @@ def test_host_entry_matches_device_entry(idk, oracle):
     d = idk.id_auto(dev(a), 9, idk.RANDOMIZED, seed=5, p=3)
     assert np.array_equal(h.cols, host(d.cols)) and np.array_equal(h.z, host(d.z))
     assert np.array_equal(h.c, host(d.c))
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_pipelined_host_entry_matches_single_calls(idk, oracle, method):
+    mats = [oracle.gaussian_matrix(60, 90, s) for s in range(6)]
+    mats = [np.asfortranarray(x) for x in mats]
+    cols, zs, cs, tr = idk.id_auto_many(mats, 8, method, seed=3, p=4)
+    assert not tr
+    tall = [np.asfortranarray(oracle.gaussian_matrix(90, 60, s)) for s in range(3)]
+    tcols, tzs, tcs, ttr = idk.id_auto_many(tall, 8, method, seed=3, p=4)
+    assert ttr
+    for x, c_, z_ in zip(tall, tcols, tzs):
+        r = idk.id_auto(x, 8, method, seed=3, p=4)
+        assert np.array_equal(c_, r.cols) and np.array_equal(z_, r.z)
+    for x, c_, z_, cc in zip(mats, cols, zs, cs):
+        r = idk.id_auto(x, 8, method, seed=3, p=4)
+        assert np.array_equal(c_, r.cols) and np.array_equal(z_, r.z) and np.array_equal(cc, r.c)
+
+
+def test_pipelined_host_entry_reports_failing_index(idk, oracle):
+    good = oracle.gaussian_matrix(10, 12, 1)
+    bad = np.zeros((10, 12))
+    g = oracle.gaussian_matrix(10, 2, 8)
+    bad[:, 3], bad[:, 9] = g[:, 0], g[:, 1]
+    with pytest.raises(idk.NotPositiveDefiniteError, match="matrix 2"):
+        idk.id_auto_many([good, good, bad, good], 3, idk.DETERMINISTIC)
