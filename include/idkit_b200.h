@@ -171,6 +171,20 @@ IDK_API int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, in
 IDK_API int idk_select_columns(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, const int64_t* d_cols,
                        int64_t ncols, int rows_of_a, double* d_out);
 
+/* IdResult::approx (id.hpp:17-22, id.cpp:42,73): out (m x n, ldo) = C (m x k,
+ * ld = m) * Z (k x n, ld = k) on the DMMA pipe. */
+IDK_API int idk_approx(idk_handle h, const double* d_c, int64_t m, int64_t k, const double* d_z, int64_t n,
+                       double* d_out, int64_t ldo);
+
+/* idkit::diagnostics (id.hpp:60, id.cpp:97-122) of a device result for the
+ * stored m x n matrix A: h_out4 = {relative_error, max_abs_z,
+ * identity_deviation, entry_bound_satisfied (0/1)}.  ||A - approx||_F is
+ * computed inside the C*Z GEMM epilogue, so approx is never materialised.
+ * transposed != 0: the dual result of id_auto (cols index rows, Z is k x m).
+ * d_c may be NULL (gathered here). */
+IDK_API int idk_diagnostics(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int transposed,
+                            const int64_t* d_cols, int64_t k, const double* d_z, const double* d_c, double* h_out4);
+
 /* ---- host-buffer entries (the reference's value-semantics calls) ------------ */
 
 /* Same as idk_id_auto, host pointers in and out; host<->device copies are

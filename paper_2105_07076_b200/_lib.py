@@ -38,6 +38,8 @@ SIGNATURES = {
     "idk_sketch": (C.c_int, [_P, _P, _I64, _P, _I64, _I64, _I64, C.c_int, _P, _I64]),
     "idk_qr_column_pivoted": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "idk_select_columns": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, C.c_int, _P]),
+    "idk_approx": (C.c_int, [_P, _P, _I64, _I64, _P, _I64, _P, _I64]),
+    "idk_diagnostics": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _P, _I64, _P, _P, C.POINTER(C.c_double)]),
     "idk_id_auto_host_many": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P,
                                         C.POINTER(C.c_int)]),
     "idk_id_auto_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P,

@@ -618,6 +618,59 @@ int idk_id_from_sketch(idk_handle h, double* d_y, int64_t l, int64_t n, int64_t 
     return IDK_OK;
 }
 
+int idk_approx(idk_handle h, const double* d_c, int64_t m, int64_t k, const double* d_z, int64_t n, double* d_out,
+               int64_t ldo) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (m <= 0 || n <= 0 || k <= 0 || m > INT_MAX || ldo < m || !d_c || !d_z || !d_out)
+        return set_err(h, IDK_ERR_INVALID_ARG, "approx: bad arguments");
+    IDK_CUDA(idk::sketch_gemm(d_c, m, d_z, k, false, d_out, ldo, static_cast<int>(m), n, k, 1, nullptr, h->stream));
+    h->launches += 1;
+    return IDK_OK;
+}
+
+int idk_diagnostics(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int transposed,
+                    const int64_t* d_cols, int64_t k, const double* d_z, const double* d_c, double* h_out4) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (m <= 0 || n <= 0 || k <= 0 || lda < m || !d_a || !d_cols || !d_z || !h_out4)
+        return set_err(h, IDK_ERR_INVALID_ARG, "diagnostics: bad arguments");
+    // M: the decomposed matrix (A, or A^T for the dual); C is M's column subset.
+    const int64_t mr = transposed ? n : m, mc = transposed ? m : n;
+    if (mr > INT_MAX) return set_err(h, IDK_ERR_INVALID_ARG, "diagnostics: dimension too large");
+    Carve cv;
+    const size_t cofs = d_c ? 0 : cv.take(sizeof(double) * mr * k);
+    const size_t pofs = cv.take(sizeof(double) * idk::resid_partials(static_cast<int>(mr), mc));
+    const size_t oofs = cv.take(sizeof(double) * 4);
+    int rc;
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    const double* c = d_c;
+    if (!c) {
+        double* cc = reinterpret_cast<double*>(h->ws + cofs);
+        IDK_CUDA(idk::gather_columns(d_a, lda, mr, reinterpret_cast<const long long*>(d_cols), static_cast<int>(k),
+                                     transposed != 0, cc, h->stream));
+        h->launches += 1;
+        c = cc;
+    }
+    double* out = reinterpret_cast<double*>(h->ws + oofs);
+    // ||A - C Z||_F without materialising approx (fused into the DMMA GEMM epilogue);
+    // for the dual, C Z is A^T's approximation: compare against A read transposed.
+    IDK_CUDA(idk::gemm_residual(c, mr, d_z, k, static_cast<int>(mr), mc, k, d_a, lda, transposed != 0,
+                                reinterpret_cast<double*>(h->ws + pofs), out, h->stream));
+    IDK_CUDA(idk::z_stats(d_z, static_cast<int>(k), mc, reinterpret_cast<const long long*>(d_cols), out + 2,
+                          h->stream));
+    h->launches += 3;
+    double hv[4];
+    IDK_CUDA(cudaMemcpyAsync(hv, out, sizeof(hv), cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    const double dist = std::sqrt(hv[0]), denom = std::sqrt(hv[1]);
+    h_out4[0] = denom > 0.0 ? dist / denom : (dist > 0.0 ? INFINITY : 0.0);  // id.cpp:104-106
+    h_out4[1] = hv[2];
+    h_out4[2] = hv[3];
+    h_out4[3] = hv[2] <= 2.0 + 1e-12 ? 1.0 : 0.0;
+    return IDK_OK;
+}
+
 int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a, int64_t m, int64_t n, int64_t k,
                           int method, uint64_t seed, int64_t p, int omega_mode, int64_t* const* h_cols,
                           double* const* h_z, double* const* h_c, int* transposed) {

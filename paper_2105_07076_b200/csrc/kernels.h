@@ -13,6 +13,13 @@ int sketch_gemm_pick_splits(int M, int64_t N, int64_t K, int num_sms);
 cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans, double* Y,
                         int64_t ldc, int M, int64_t N, int64_t K, int splits, double* partial, cudaStream_t stream);
 cudaError_t omega_philox(double* out, int64_t l, int64_t m, uint64_t seed, cudaStream_t stream);
+int64_t resid_partials(int M, int64_t N);
+cudaError_t gemm_residual(const double* A, int64_t lda, const double* B, int64_t ldb, int M, int64_t N, int64_t K,
+                          const double* Ref, int64_t ldr, bool ref_trans, double* part, double* out2,
+                          cudaStream_t stream);
+
+// diag.cu
+cudaError_t z_stats(const double* Z, int k, int64_t zc, const long long* cols, double* out2, cudaStream_t stream);
 
 // cpqr.cu
 constexpr size_t kCpqrPubBytes = 32;

@@ -64,7 +64,8 @@ sketch_gemm_kernel(const double* __restrict__ A, int64_t lda,  // Omega: l x K
                    const double* __restrict__ B, int64_t ldb,  // big matrix
                    double* __restrict__ C, int64_t ldc,        // Y (or split-K partial base)
                    int64_t split_stride,                       // elements between split partials
-                   int M, int64_t N, int64_t K, int64_t k_per_split, bool vec16) {
+                   int M, int64_t N, int64_t K, int64_t k_per_split, bool vec16,
+                   const double* __restrict__ Ref, int64_t ldr, bool ref_trans, double* __restrict__ resid) {
     using S = Smem<WM, kNT>;
     constexpr int BM = S::BM;
     extern __shared__ __align__(16) double smem[];
@@ -187,6 +188,38 @@ sketch_gemm_kernel(const double* __restrict__ A, int64_t lda,  // Omega: l x K
     }
     cp_async_wait<0>();
 
+    if (Ref != nullptr) {
+        // Fused residual (id.cpp:97-122 diagnostics without materialising
+        // approx): sum (Ref - A*B)^2 and sum Ref^2 over this tile, one pair
+        // of partials per warp, reduced in a fixed order afterwards.
+        double dsum = 0.0, rsum = 0.0;
+#pragma unroll
+        for (int tm = 0; tm < WM; ++tm) {
+            const int i = m0 + wm * (8 * WM) + tm * 8 + fr;
+#pragma unroll
+            for (int tn = 0; tn < 4; ++tn) {
+                const int64_t j = n0 + wn * 32 + tn * 8 + 2 * fc;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (i < M && j + u < N) {
+                        const double r = ref_trans ? Ref[static_cast<int64_t>(i) * ldr + j + u] : Ref[(j + u) * ldr + i];
+                        const double d = r - acc[tm][tn][u];
+                        dsum = fma(d, d, dsum);
+                        rsum = fma(r, r, rsum);
+                    }
+                }
+            }
+        }
+        dsum = warp_sum(dsum);
+        rsum = warp_sum(rsum);
+        if (lane == 0) {
+            const int64_t cta = blockIdx.x + static_cast<int64_t>(gridDim.x) * (blockIdx.y + static_cast<int64_t>(gridDim.y) * blockIdx.z);
+            resid[(cta * 4 + warp) * 2] = dsum;
+            resid[(cta * 4 + warp) * 2 + 1] = rsum;
+        }
+        return;
+    }
+
 #pragma unroll
     for (int tm = 0; tm < WM; ++tm) {
         const int i = m0 + wm * (8 * WM) + tm * 8 + fr;
@@ -218,7 +251,8 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ P, int64_t split
 template <int WM, bool kNT>
 cudaError_t launch_wm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K, int splits,
-                      bool vec16, cudaStream_t stream) {
+                      bool vec16, cudaStream_t stream, const double* Ref = nullptr, int64_t ldr = 0,
+                      bool ref_trans = false, double* resid = nullptr) {
     using S = Smem<WM, kNT>;
     auto kern = sketch_gemm_kernel<WM, kNT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -228,7 +262,7 @@ cudaError_t launch_wm(const double* A, int64_t lda, const double* B, int64_t ldb
     kps = ((kps + kBK - 1) / kBK) * kBK;
     dim3 grid((M + S::BM - 1) / S::BM, static_cast<unsigned>((N + kBN - 1) / kBN), splits);
     kern<<<grid, kThreads, S::BYTES, stream>>>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, kps,
-                                               vec16);
+                                               vec16, Ref, ldr, ref_trans, resid);
     return cudaGetLastError();
 }
 
@@ -247,6 +281,34 @@ cudaError_t launch_nt(int wm, const double* A, int64_t lda, const double* B, int
 }
 
 }  // namespace
+
+// Fixed-order sum of the residual partials: out[0] = sum (Ref - AB)^2, out[1] = sum Ref^2.
+__global__ void resid_reduce_kernel(const double* __restrict__ part, int64_t count, double* __restrict__ out) {
+    __shared__ double sd[32], sr[32];
+    double d = 0.0, r = 0.0;
+    for (int64_t e = threadIdx.x; e < count; e += blockDim.x) {
+        d += part[2 * e];
+        r += part[2 * e + 1];
+    }
+    d = warp_sum(d);
+    r = warp_sum(r);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        sd[wid] = d;
+        sr[wid] = r;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        d = lane < static_cast<int>(blockDim.x >> 5) ? sd[lane] : 0.0;
+        r = lane < static_cast<int>(blockDim.x >> 5) ? sr[lane] : 0.0;
+        d = warp_sum(d);
+        r = warp_sum(r);
+        if (lane == 0) {
+            out[0] = d;
+            out[1] = r;
+        }
+    }
+}
 
 // Pick BM = 16*WM (WM in 2..7) minimising padded rows over ceil(M/BM) tiles.
 int sketch_gemm_pick_wm(int M) {
@@ -291,6 +353,35 @@ cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t l
     const int64_t total = static_cast<int64_t>(M) * N;
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
     splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(partial, split_stride, splits, Y, M, N, ldc);
+    return cudaGetLastError();
+}
+
+// Residual of a product: out2 = {||Ref - A*B||_F^2, ||Ref||_F^2} with A (M x K,
+// lda) and B (K x N, ldb); Ref is M x N (ldr) or, with ref_trans, N x M.
+// `part` needs resid_partials(M, N) doubles.
+int64_t resid_partials(int M, int64_t N) {
+    const int wm = sketch_gemm_pick_wm(M);
+    const int64_t ctas = ((M + 16 * wm - 1) / (16 * wm)) * ((N + kBN - 1) / kBN);
+    return ctas * 4 * 2;
+}
+
+cudaError_t gemm_residual(const double* A, int64_t lda, const double* B, int64_t ldb, int M, int64_t N, int64_t K,
+                          const double* Ref, int64_t ldr, bool ref_trans, double* part, double* out2,
+                          cudaStream_t stream) {
+    const int wm = sketch_gemm_pick_wm(M);
+    const bool vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+    cudaError_t e;
+    switch (wm) {
+        case 2: e = launch_wm<2, false>(A, lda, B, ldb, nullptr, 0, 0, M, N, K, 1, vec16, stream, Ref, ldr, ref_trans, part); break;
+        case 3: e = launch_wm<3, false>(A, lda, B, ldb, nullptr, 0, 0, M, N, K, 1, vec16, stream, Ref, ldr, ref_trans, part); break;
+        case 4: e = launch_wm<4, false>(A, lda, B, ldb, nullptr, 0, 0, M, N, K, 1, vec16, stream, Ref, ldr, ref_trans, part); break;
+        case 5: e = launch_wm<5, false>(A, lda, B, ldb, nullptr, 0, 0, M, N, K, 1, vec16, stream, Ref, ldr, ref_trans, part); break;
+        case 6: e = launch_wm<6, false>(A, lda, B, ldb, nullptr, 0, 0, M, N, K, 1, vec16, stream, Ref, ldr, ref_trans, part); break;
+        default: e = launch_wm<7, false>(A, lda, B, ldb, nullptr, 0, 0, M, N, K, 1, vec16, stream, Ref, ldr, ref_trans, part); break;
+    }
+    if (e != cudaSuccess) return e;
+    resid_reduce_kernel<<<1, 1024, 0, stream>>>(part, resid_partials(M, N) / 2, out2);
     return cudaGetLastError();
 }
 

@@ -324,6 +324,37 @@ def id_from_sketch(y, k: int, c_begin: int = 0, c_end: Optional[int] = None):
     return cols, z
 
 
+def approx(r: IdResult):
+    """IdResult::approx (id.hpp:17-22) on the device: C Z, or (C Z)^T for the dual."""
+    import torch
+    c, z = fortran(r.c), fortran(r.z)
+    mr, k = c.shape
+    n = z.shape[1]
+    ctx = context(c.device.index or 0)
+    ctx.bind_stream()
+    out = empty_f(mr, n, c.device)
+    ctx.check(ctx.lib.idk_approx(ctx.h, _ptr(c), mr, k, _ptr(z), n, _ptr(out), mr))
+    return out.t() if r.transposed else out
+
+
+def diagnostics(a, r: IdResult) -> dict:
+    """idkit::diagnostics (id.hpp:60): relative error, max |Z|, identity
+    deviation, |Z| <= 2 flag -- on the device, approx never materialised."""
+    a = fortran(a)
+    m, n = a.shape
+    z = fortran(r.z)
+    cols = r.cols.contiguous()
+    k = cols.numel()
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    out = (C.c_double * 4)()
+    cptr = _ptr(fortran(r.c)) if r.c is not None else None
+    ctx.check(ctx.lib.idk_diagnostics(ctx.h, _ptr(a), m, n, _ld(a), 1 if r.transposed else 0, _ptr(cols), k,
+                                      _ptr(z), cptr, out))
+    return {"relative_error": out[0], "max_abs_z": out[1], "identity_deviation": out[2],
+            "entry_bound_satisfied": bool(out[3])}
+
+
 # ---- stages / primitives ----------------------------------------------------------
 
 def sketch_omega(l: int, m: int, seed: int, device=0):

@@ -325,3 +325,23 @@ def test_pipelined_host_entry_reports_failing_index(idk, oracle):
     bad[:, 3], bad[:, 9] = g[:, 0], g[:, 1]
     with pytest.raises(idk.NotPositiveDefiniteError, match="matrix 2"):
         idk.id_auto_many([good, good, bad, good], 3, idk.DETERMINISTIC)
+
+
+@pytest.mark.parametrize("shape,k,method", [((40, 70), 9, 0), ((300, 500), 40, 1), ((900, 120), 16, 1), ((120, 90), 7, 0)])
+def test_diagnostics_and_approx_match_reference(idk, ref, shape, k, method):
+    """id.cpp:97-122 on the device (fused residual) vs the reference's diagnostics."""
+    a = ref.gaussian_matrix(shape[0], shape[1], 21)
+    r = idk.id_auto(dev(a), k, method, seed=4, p=3)
+    d = idk.diagnostics(dev(a), r)
+    ap = host(idk.approx(r))
+    cols, z = host(r.cols), host(r.z)
+    rd = ref.diagnostics(a, cols, z, ap)
+    assert abs(d["relative_error"] - rd["relative_error"]) <= 1e-12 * max(rd["relative_error"], 1e-300)
+    assert d["max_abs_z"] == rd["max_abs_z"]
+    assert abs(d["identity_deviation"] - rd["identity_deviation"]) <= 1e-15
+    assert d["entry_bound_satisfied"] == rd["entry_bound_satisfied"]
+    if r.transposed:
+        want = z.T @ a[cols, :]
+    else:
+        want = a[:, cols] @ z
+    assert rel(ap, want) <= 1e-13
