@@ -120,10 +120,25 @@ IDK_API int idk_sketch_rid(idk_handle h, const double* d_a, int64_t m, int64_t n
                    int64_t k, int64_t p, uint64_t seed, int omega_mode, const double* d_omega,
                    int64_t* d_cols, double* d_z, double* d_c);
 
+/* The reference's randomized ID, idkit::optim_rid (id.hpp:47-50, id.cpp:47-76):
+ * sample p = min(k + floor(fraction * k), n) columns of M without replacement
+ * (mt19937_64(seed), partial Fisher-Yates, random.cpp:29-41 -- bit-identical
+ * to the reference's sample), CPQR of M[:, S] (k steps), cols = S[perm[:k]],
+ * C = M[:, cols], Z = (R_k^T R_k)^-1 C^T M by Bunch-Kaufman LDL^T
+ * (solve_symmetric_indefinite, solve.cpp:262-274).  M = A or A^T as in
+ * idk_sketch_rid.  A singular pivot block -> IDK_ERR_SINGULAR (the
+ * reference's SingularMatrixError, test_id.cpp:109-118); fraction < 0 ->
+ * IDK_ERR_INVALID_ARG. */
+IDK_API int idk_optim_rid(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int a_transposed,
+                          int64_t k, double oversampling_fraction, uint64_t seed, int64_t* d_cols, double* d_z,
+                          double* d_c);
+
 /* Orientation dispatch, idkit::id_auto (id.hpp:55-56, id.cpp:78-95): A is
  * m x n; if m <= n the ID runs on A, else on A^T with *transposed = 1, cols
  * indexing rows of A and Z being k x m.  method 0 = deterministic
- * (idk_optim_id), 1 = Gaussian-sketch RID (idk_sketch_rid).  d_z must hold
+ * (idk_optim_id), 1 = Gaussian-sketch RID (idk_sketch_rid), 2 = the
+ * reference's column-sampling RID (idk_optim_rid) with p = floor(fraction * k)
+ * extra sampled columns (id.cpp:54).  d_z must hold
  * k * max(m, n) doubles; d_c (optional) m x k or n x k accordingly. */
 IDK_API int idk_id_auto(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int method,
                 uint64_t seed, int64_t p, int omega_mode, const double* d_omega, int64_t* d_cols,

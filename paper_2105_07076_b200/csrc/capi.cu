@@ -34,6 +34,8 @@ struct idk_context {
     int* h_status = nullptr;  // pinned
     double* h_omega = nullptr;  // pinned staging for IDK_OMEGA_MT19937
     size_t h_omega_cap = 0;
+    long long* h_idx = nullptr;  // pinned staging for optim_rid's sampled columns
+    size_t h_idx_cap = 0;
     int64_t launches = 0;
     int cpqr_mode = IDK_CPQR_AUTO;
     bool batched_exact = false;
@@ -312,14 +314,124 @@ int sketch_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t 
     return factor_and_solve(h, ch, Y, l, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, false);
 }
 
+// sample_without_replacement(population, count, seeded_engine(seed))
+// (random.cpp:17-41): partial Fisher-Yates over mt19937_64 with the
+// reference's rejection rule for next_below.  O(count) engine draws on the
+// host -- the column indices, not the matrix, are what crosses PCIe.
+void host_sample_columns(long long* out, int64_t population, int64_t count, uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    std::vector<long long> pool(static_cast<size_t>(population));
+    for (int64_t i = 0; i < population; ++i) pool[static_cast<size_t>(i)] = i;
+    for (int64_t i = 0; i < count; ++i) {
+        const uint64_t bound = static_cast<uint64_t>(population - i);
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+        uint64_t x;
+        do {
+            x = rng();
+        } while (x >= limit);
+        std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(i + static_cast<int64_t>(x % bound))]);
+    }
+    std::memcpy(out, pool.data(), sizeof(long long) * static_cast<size_t>(count));
+}
+
+// The reference's own randomized ID, idkit::optim_rid (id.cpp:47-76):
+// sample p = min(k + extra, n) columns of M, CPQR(M[:, S], k),
+// cols = S[perm[:k]], C = M[:, cols], Z = solve_symmetric_indefinite(
+// R_k^T R_k, C^T M) (Bunch-Kaufman LDL^T).  M = A or A^T as in sketch_rid.
+int sampled_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda, bool trans, int64_t k,
+                int64_t extra, uint64_t seed, int64_t* d_cols, double* d_z, double* d_c) {
+    int rc = check_k(h, m, n, k, "optim_rid");
+    if (rc) return rc;
+    if (extra < 0) return set_err(h, IDK_ERR_INVALID_ARG, "optim_rid: oversampling_fraction must be non-negative");
+    if (!d_a || !d_cols || !d_z) return set_err(h, IDK_ERR_INVALID_ARG, "optim_rid: null pointer");
+    if (lda < (trans ? n : m)) return set_err(h, IDK_ERR_INVALID_ARG, "optim_rid: lda too small");
+    const int64_t p = std::min(k + extra, n);
+    const CpqrChoice ch = choose_cpqr(h, m, p, k);
+    if ((rc = check_cpqr_fits(h, m, p, ch))) return rc;
+    const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(k), n, m, h->num_sms);
+    Carve cv;
+    const size_t sofs = cv.take(sizeof(long long) * p);
+    const size_t wofs = cv.take(sizeof(double) * m * p);
+    const CpqrWs w = carve_cpqr(cv, m, p, k, h->num_sms, ch);
+    const size_t cofs = d_c ? 0 : cv.take(sizeof(double) * m * k);
+    const size_t ctofs = cv.take(sizeof(double) * m * k);
+    const size_t rtofs = cv.take(sizeof(double) * k * k);
+    const size_t gofs = cv.take(sizeof(double) * k * k);
+    const size_t fofs = cv.take(sizeof(double) * k * k);
+    const size_t lofs = cv.take(idk::ldlt_scratch_bytes(static_cast<int>(k)));
+    const size_t pofs = splits > 1 ? cv.take(sizeof(double) * k * n * splits) : 0;
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    char* base = h->ws;
+    long long* sampled = reinterpret_cast<long long*>(base + sofs);
+    double* W = reinterpret_cast<double*>(base + wofs);
+    long long* piv = reinterpret_cast<long long*>(base + w.pivots);
+    int* status = reinterpret_cast<int*>(base + w.status);
+    double* C = d_c ? d_c : reinterpret_cast<double*>(base + cofs);
+    double* Ct = reinterpret_cast<double*>(base + ctofs);
+    double* R11 = reinterpret_cast<double*>(base + w.r11);
+    double* R11t = reinterpret_cast<double*>(base + rtofs);
+    double* gram = reinterpret_cast<double*>(base + gofs);
+    double* F = reinterpret_cast<double*>(base + fofs);
+    const int ki = static_cast<int>(k);
+
+    const size_t idx_bytes = sizeof(long long) * p;
+    if (idx_bytes > h->h_idx_cap) {
+        cudaStreamSynchronize(h->stream);
+        if (h->h_idx) cudaFreeHost(h->h_idx);
+        h->h_idx = nullptr;
+        h->h_idx_cap = 0;
+        IDK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->h_idx), idx_bytes));
+        h->h_idx_cap = idx_bytes;
+    }
+    IDK_CUDA(cudaStreamSynchronize(h->stream));  // the staging buffer may still be in flight
+    host_sample_columns(h->h_idx, n, p, seed);
+    mark(h, 0);
+    IDK_CUDA(cudaMemcpyAsync(sampled, h->h_idx, idx_bytes, cudaMemcpyHostToDevice, h->stream));
+    IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
+    IDK_CUDA(idk::gather_columns(d_a, lda, m, sampled, static_cast<int>(p), trans, W, h->stream));
+    mark(h, 1);
+    mark(h, 2);
+    IDK_CUDA(run_cpqr(h, ch, W, m, p, k, base, w));
+    mark(h, 3);
+    IDK_CUDA(idk::map_cols(sampled, piv, ki, reinterpret_cast<long long*>(d_cols), h->stream));
+    IDK_CUDA(idk::gather_columns(d_a, lda, m, reinterpret_cast<const long long*>(d_cols), ki, trans, C, h->stream));
+    // gram = R_k^T R_k, rhs = C^T M (written straight into Z), both on the DMMA pipe
+    IDK_CUDA(idk::gather_r11(W, m, piv, ki, R11, h->stream));
+    IDK_CUDA(idk::transpose_copy(R11, k, k, k, R11t, k, h->stream));
+    IDK_CUDA(idk::sketch_gemm(R11t, k, R11, k, false, gram, k, ki, k, k, 1, nullptr, h->stream));
+    IDK_CUDA(idk::transpose_copy(C, m, m, k, Ct, k, h->stream));
+    IDK_CUDA(idk::sketch_gemm(Ct, k, d_a, lda, trans, d_z, k, ki, n, m, splits,
+                              splits > 1 ? reinterpret_cast<double*>(base + pofs) : nullptr, h->stream));
+    IDK_CUDA(idk::ldlt_factor(gram, ki, F, base + lofs, status, h->stream));
+    IDK_CUDA(idk::ldlt_solve(F, base + lofs, ki, n, d_z, h->stream));
+    mark(h, 4);
+    mark(h, 5);
+    h->launches += 11 + (splits > 1 ? 1 : 0);
+    if (h->async_status) {
+        IDK_CUDA(cudaMemcpyAsync(h->async_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        return IDK_OK;
+    }
+    IDK_CUDA(cudaMemcpyAsync(h->h_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    collect_stage_times(h);
+    const int bad = *h->h_status;
+    if (bad != 0x7f7f7f7f)
+        return set_err(h, IDK_ERR_SINGULAR,
+                       "solve_symmetric_indefinite: zero pivot block at index " + std::to_string(bad));
+    return IDK_OK;
+}
+
 int id_auto_dev(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int method,
                 uint64_t seed, int64_t p, int omega_mode, const double* d_omega, int64_t* d_cols, double* d_z,
                 double* d_c, int* transposed) {
     int rc = check_k(h, m, n, k, "id_auto");
     if (rc) return rc;
-    if (method != 0 && method != 1) return set_err(h, IDK_ERR_INVALID_ARG, "id_auto: method must be 0 or 1");
+    if (method < 0 || method > 2) return set_err(h, IDK_ERR_INVALID_ARG, "id_auto: method must be 0, 1 or 2");
     const bool tall = m > n;
     if (transposed) *transposed = tall ? 1 : 0;
+    if (method == 2)  // the reference's column-sampling optim_rid, extra = floor(fraction * k) columns
+        return tall ? sampled_rid(h, d_a, n, m, lda, true, k, p, seed, d_cols, d_z, d_c)
+                    : sampled_rid(h, d_a, m, n, lda, false, k, p, seed, d_cols, d_z, d_c);
     if (!tall) {
         return method == 0 ? det_id(h, d_a, m, n, lda, false, k, d_cols, d_z, d_c)
                            : sketch_rid(h, d_a, m, n, lda, false, k, p, seed, omega_mode, d_omega, d_cols, d_z, d_c);
@@ -378,6 +490,7 @@ int idk_destroy(idk_handle h) {
     if (h->io) cudaFree(h->io);
     if (h->h_status) cudaFreeHost(h->h_status);
     if (h->h_omega) cudaFreeHost(h->h_omega);
+    if (h->h_idx) cudaFreeHost(h->h_idx);
     if (h->h_status_many) cudaFreeHost(h->h_status_many);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
@@ -464,6 +577,18 @@ int idk_sketch_rid(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_
     if (!h) return IDK_ERR_INVALID_ARG;
     cudaSetDevice(h->device);
     return sketch_rid(h, d_a, m, n, lda, a_transposed != 0, k, p, seed, omega_mode, d_omega, d_cols, d_z, d_c);
+}
+
+int idk_optim_rid(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int a_transposed, int64_t k,
+                  double oversampling_fraction, uint64_t seed, int64_t* d_cols, double* d_z, double* d_c) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (!(oversampling_fraction >= 0.0))
+        return set_err(h, IDK_ERR_INVALID_ARG, "optim_rid: oversampling_fraction must be non-negative");
+    // p = k + size_t(fraction * k) (id.cpp:54); the clamp to n happens inside
+    const double extra = oversampling_fraction * static_cast<double>(k);
+    const int64_t e = extra >= 9.0e18 ? INT64_MAX / 2 : static_cast<int64_t>(static_cast<uint64_t>(extra));
+    return sampled_rid(h, d_a, m, n, lda, a_transposed != 0, k, e, seed, d_cols, d_z, d_c);
 }
 
 int idk_id_auto(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t k, int method,

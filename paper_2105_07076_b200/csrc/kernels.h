@@ -53,6 +53,8 @@ cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int
                        const long long* pos, double* R11, int* status, double* Z, cudaStream_t stream);
 cudaError_t gather_columns(const double* A, int64_t lda, int64_t rows, const long long* cols, int k, bool rows_of_a,
                            double* C, cudaStream_t stream);
+cudaError_t gather_r11(const double* W, int64_t ldw, const long long* pivots, int k, double* R11,
+                       cudaStream_t stream);
 cudaError_t copy_pivots(const long long* src, int k, long long* dst, cudaStream_t stream);
 
 // batched.cu
@@ -65,6 +67,12 @@ size_t batched_fast_smem_bytes(int n, int k);
 bool batched_fast_ok(const double* A, int64_t lda, int64_t stride, int m, int n, int k, size_t smem_optin);
 cudaError_t batched_id_fast(const double* A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
                             long long* cols, double* Z, double* C, int* status, int num_sms, cudaStream_t stream);
+
+// ldlt.cu (optim_rid's symmetric-indefinite solve)
+size_t ldlt_scratch_bytes(int k);
+cudaError_t ldlt_factor(const double* S, int k, double* F, void* scratch, int* status, cudaStream_t stream);
+cudaError_t ldlt_solve(const double* F, const void* scratch, int k, int64_t n, double* B, cudaStream_t stream);
+cudaError_t map_cols(const long long* sampled, const long long* piv, int k, long long* cols, cudaStream_t stream);
 
 // util.cu
 cudaError_t transpose_copy(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb,

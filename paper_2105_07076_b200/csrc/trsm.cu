@@ -30,7 +30,7 @@ __global__ void gather_r11_kernel(const double* __restrict__ W, int64_t ldw, con
         const int j = static_cast<int>(e / k), i = static_cast<int>(e % k);
         const double v = (i <= j) ? W[pivots[j] * ldw + i] : 0.0;
         R11[e] = v;
-        if (i == j && fabs(v) <= 1e-300) atomicMin(status, j);
+        if (status && i == j && fabs(v) <= 1e-300) atomicMin(status, j);
     }
 }
 
@@ -315,6 +315,14 @@ cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int
     const int nb2 = id_trsm_nb(k);
     const int64_t blocks = (n + nb2 - 1) / nb2;
     id_trsm_kernel<<<static_cast<unsigned>(blocks), kTrsmThreads, smem, stream>>>(W, ldw, R11, k, n, pos, Z, nb2);
+    return cudaGetLastError();
+}
+
+cudaError_t gather_r11(const double* W, int64_t ldw, const long long* pivots, int k, double* R11,
+                       cudaStream_t stream) {
+    const int64_t kk = static_cast<int64_t>(k) * k;
+    gather_r11_kernel<<<static_cast<int>(std::min<int64_t>((kk + 255) / 256, 1024)), 256, 0, stream>>>(
+        W, ldw, pivots, k, R11, nullptr);
     return cudaGetLastError();
 }
 

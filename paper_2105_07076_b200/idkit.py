@@ -30,7 +30,7 @@ import numpy as np
 from . import _lib
 
 OMEGA_PHILOX, OMEGA_MT19937, OMEGA_VERBATIM = 0, 1, 2
-DETERMINISTIC, RANDOMIZED = 0, 1
+DETERMINISTIC, RANDOMIZED, SAMPLED = 0, 1, 2  # SAMPLED: the reference's column-sampling optim_rid
 
 
 class IdkitError(RuntimeError):
@@ -226,10 +226,43 @@ def sketch_rid(a, k: int, p: int, seed: int = 0, omega_mode: int = OMEGA_PHILOX,
     return IdResult(cols, z, c, transposed)
 
 
+def optim_rid(a, k: int, oversampling_fraction: float = 0.2, seed: int = 0, transposed: bool = False,
+              want_c: bool = True) -> IdResult:
+    """The reference's randomized ID (id.hpp:47-50, id.cpp:47-76): column sampling
+    (mt19937_64, bit-identical sample) -> CPQR of A[:, S] -> Bunch-Kaufman solve
+    of (R_k^T R_k) Z = C^T A.  Singular sample -> SingularMatrixError."""
+    import torch
+    if not is_torch(a):
+        r = optim_rid(torch.from_numpy(np.asfortranarray(a, dtype=np.float64)).cuda(), k, oversampling_fraction,
+                      seed, transposed, want_c)
+        return IdResult(r.cols.cpu().numpy(), r.z.cpu().numpy(), None if r.c is None else r.c.cpu().numpy(),
+                        transposed)
+    a = fortran(a)
+    n, m = a.shape if transposed else a.shape[::-1]
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    cols = torch.empty(max(k, 0), dtype=torch.int64, device=a.device)
+    z = empty_f(max(k, 0), n, a.device)
+    c = empty_f(m, max(k, 0), a.device) if want_c else None
+    ctx.check(ctx.lib.idk_optim_rid(ctx.h, _ptr(a), m, n, _ld(a), 1 if transposed else 0, k,
+                                    float(oversampling_fraction), seed, _ptr(cols), _ptr(z), _ptr(c)))
+    return IdResult(cols, z, c, transposed)
+
+
+def _sampled_extra(k: int, frac: float) -> int:
+    if not frac >= 0.0:
+        raise InvalidArgument("optim_rid: oversampling_fraction must be non-negative")
+    return int(float(frac) * float(k))  # size_t(fraction * k), id.cpp:54
+
+
 def id_auto(a, k: int, method: int = DETERMINISTIC, seed: int = 0, p: int = 0,
-            omega_mode: int = OMEGA_PHILOX, want_c: bool = True) -> IdResult:
+            omega_mode: int = OMEGA_PHILOX, want_c: bool = True, oversampling_fraction: float = None) -> IdResult:
     """id.hpp:55-56: tall inputs (m > n) are decomposed through their transpose.
-    `p` is the sketch oversampling (rows of Omega = k + p) for method=RANDOMIZED."""
+    `p` is the sketch oversampling (rows of Omega = k + p) for method=RANDOMIZED;
+    method=SAMPLED runs the reference's optim_rid with `oversampling_fraction`
+    (default 0.2, id.hpp:56)."""
+    if method == SAMPLED:
+        p = _sampled_extra(k, 0.2 if oversampling_fraction is None else oversampling_fraction)
     m, n = a.shape
     tall = m > n
     zc = m if tall else n
