@@ -64,7 +64,9 @@ typedef enum {
 typedef enum {
     IDK_CPQR_AUTO = 0,           /* resident, single cluster when it fits, else resident grid, else streaming */
     IDK_CPQR_RESIDENT_GRID = 1,  /* resident in registers + shared memory, one CTA per SM, grid exchange      */
-    IDK_CPQR_STREAMING = 2       /* trailing matrix streamed through L2 every step (any shape)               */
+    IDK_CPQR_STREAMING = 2,      /* trailing matrix streamed through L2 every step (any shape)               */
+    IDK_CPQR_CLUSTER_PULL = 3    /* single cluster, winner column pulled over DSMEM (the large-m fallback
+                                    of AUTO's cluster push exchange; selectable for testing)                 */
 } idk_cpqr_mode;
 
 /* ---- handle ---------------------------------------------------------------- */
@@ -83,12 +85,12 @@ IDK_API int idk_set_cpqr_mode(idk_handle h, int mode);
  * unfused IEEE ops); 0 (default) = the throughput kernel (registers + TMA
  * prefetch + FMA), which matches within rounding. */
 IDK_API int idk_set_batched_exact(idk_handle h, int exact);
-/* The CPQR plan for an m x n, k-step factorisation: out8 = {kind (1 cluster,
- * 2 resident grid, 3 streaming), CTAs, columns per CTA, threads per column,
+/* The CPQR plan for an m x n, k-step factorisation: out8 = {kind (1 cluster push,
+ * 2 resident grid, 3 streaming, 4 cluster pull), CTAs, columns per CTA, threads per column,
  * register rows per thread, shared-memory rows, threads per CTA, smem bytes}. */
 IDK_API int idk_cpqr_plan(idk_handle h, int64_t m, int64_t n, int64_t k, int64_t* out8);
-/* Debug: record clock64() at 8 phase marks per CPQR step (CTA 0) into d_buf
- * (k*8 int64, device); NULL turns it off.  Process-wide. */
+/* Debug: record %globaltimer at up to 16 phase marks per CPQR step (CTA 0) into d_buf
+ * (k*16 int64 per CTA, device); NULL turns it off.  Process-wide. */
 IDK_API int idk_debug_cpqr_trace(idk_handle h, int64_t* d_buf);
 /* Record CUDA events at stage boundaries on the handle's stream. */
 IDK_API int idk_set_profiling(idk_handle h, int enable);

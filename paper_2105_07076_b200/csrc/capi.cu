@@ -136,8 +136,8 @@ struct CpqrChoice {
 CpqrChoice choose_cpqr(idk_context* h, int64_t mrows, int64_t n, int64_t k) {
     CpqrChoice c;
     if (h->cpqr_mode == IDK_CPQR_STREAMING) return c;
-    c.plan = idk::cpqr_resident_plan(static_cast<int>(mrows), n, static_cast<int>(k), h->num_sms,
-                                     h->cpqr_mode != IDK_CPQR_RESIDENT_GRID);
+    const int pref = h->cpqr_mode == IDK_CPQR_RESIDENT_GRID ? 1 : (h->cpqr_mode == IDK_CPQR_CLUSTER_PULL ? 2 : 0);
+    c.plan = idk::cpqr_resident_plan(static_cast<int>(mrows), n, static_cast<int>(k), h->num_sms, pref);
     cudaGetLastError();
     c.resident = c.plan.ok;
     return c;
@@ -516,7 +516,7 @@ const char* idk_last_error(idk_handle h) { return h ? h->err.c_str() : "null han
 int64_t idk_kernel_launches(idk_handle h) { return h ? h->launches : 0; }
 
 int idk_set_cpqr_mode(idk_handle h, int mode) {
-    if (!h || mode < IDK_CPQR_AUTO || mode > IDK_CPQR_STREAMING) return IDK_ERR_INVALID_ARG;
+    if (!h || mode < IDK_CPQR_AUTO || mode > IDK_CPQR_CLUSTER_PULL) return IDK_ERR_INVALID_ARG;
     h->cpqr_mode = mode;
     return IDK_OK;
 }
@@ -530,7 +530,7 @@ int idk_set_batched_exact(idk_handle h, int exact) {
 int idk_cpqr_plan(idk_handle h, int64_t m, int64_t n, int64_t k, int64_t* out8) {
     if (!h || !out8) return IDK_ERR_INVALID_ARG;
     const CpqrChoice c = choose_cpqr(h, m, n, k);
-    out8[0] = c.resident ? (c.plan.cluster ? 1 : 2) : 3;
+    out8[0] = c.resident ? (c.plan.cluster ? (c.plan.push ? 1 : 4) : 2) : 3;
     out8[1] = c.plan.G;
     out8[2] = c.plan.nc;
     out8[3] = c.plan.S;

@@ -17,16 +17,26 @@
 //   shared    : i = q + S*r',      i < l0       (rows 0 .. l0-1, stride lds)
 // so rows retire evenly across the group as the step advances.
 //
-// Exchange.  After its trailing update every CTA publishes one record (local
-// max live norm, lowest qualifying position, column id) *and that candidate
-// column's active rows*.  After one barrier every CTA reduces the G records
-// identically and copies the winner's published column into shared memory:
-// the next reflector is then built redundantly in every CTA with no second
-// round trip.  Two exchange policies share the code:
-//   kCluster = true : one thread-block cluster (<= 16 CTAs), records in shared
-//                     memory read through DSMEM, barrier.cluster per step;
-//   kCluster = false: one CTA per SM, records in global memory (L2), a
-//                     monotonic-counter grid barrier per step.
+// Step structure.  The norm downdate needs only the dot w = tau v^T y of each
+// column, so a step is: dot + downdate for every column -> CTA argmax (one
+// __syncthreads) -> exchange of the CTA candidates -> select.  Two exchange
+// policies share the code:
+//   kCluster = true : one thread-block cluster (<= 16 CTAs).  The warp holding
+//     the CTA's winner applies that column's pending update to a raw copy with
+//     all 32 lanes, builds the next reflector, stages [v | header] in its own
+//     slot and bulk-copies it (cp.async.bulk shared::cta -> shared::cluster) to
+//     every peer, completing a transaction count on the peer's mbarrier; the
+//     other warps apply their deferred trailing axpy while the copies fly.
+//     After the mbarrier wait every warp selects the winner from local shared
+//     memory and the update reads v straight from the winner's slot copy
+//     (push mode).  When G slots of m rows do not fit, only the 48-byte
+//     headers are pushed and the winner's rows are pulled over DSMEM (pull).
+//   kCluster = false: one CTA per SM (cooperative launch).  Each CTA publishes
+//     its candidate column to a global slot and an LL-style tagged record;
+//     every thread polls at most a few records (all in flight at once), then
+//     the winner's column is copied from L2.
+// Reflectors are addressed by absolute row (v_i = 0 for retired and padding
+// rows) so the row loops carry no predicates.
 #include <climits>
 #include <cstdlib>
 #include <cooperative_groups.h>
@@ -45,6 +55,7 @@ namespace idk {
 // polling the G records is the barrier; cluster mode keeps records in shared
 // memory behind barrier.cluster.
 constexpr int kHdr = 4;
+constexpr int kCHdr = 6;  // cluster slot header: col, tau, beta, scale, vmax, pos
 constexpr int kRecWords = 4;  // vmax hi | vmax lo | pos | pad
 
 struct ResidentArgs {
@@ -64,6 +75,7 @@ struct ResidentArgs {
     double* slots;            // [3][G][kHdr + m]
     unsigned* barrier;        // debug: optional grid barrier before each exchange
     long long* trace;         // optional: %globaltimer at 8 phase marks per step, every CTA
+    int push;                 // cluster: 1 = every CTA holds every candidate (push), 0 = headers only (pull)
 };
 
 namespace {
@@ -145,44 +157,92 @@ __device__ __forceinline__ void ld_relaxed_v2(const unsigned long long* p, unsig
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
+// ---- DSMEM bulk push: cp.async.bulk shared::cta -> shared::cluster with an
+// mbarrier transaction count on the receiving CTA ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned mapa_u32(unsigned addr, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void bulk_push(unsigned dst_cluster, unsigned src_cta, unsigned bytes, unsigned mbar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst_cluster), "r"(src_cta), "r"(bytes), "r"(mbar_cluster) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned a, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "IDK_MBAR_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra IDK_MBAR_WAIT_%=;\n}"
+        ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
 }  // namespace
 
 #define IDK_REP32(M) \
     M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) \
     M(16) M(17) M(18) M(19) M(20) M(21) M(22) M(23) M(24) M(25) M(26) M(27) M(28) M(29) M(30) M(31)
 
-// xv holds the reflector at offset kGuard, with kGuard zeros in front and
-// zeros after the active length: a retired row (i < s) or a padding row
-// (i >= m) then reads v = 0, so the row loops need no predicates and every
-// lane of a warp takes the same path (the start row depends only on s).
-constexpr int kGuard = 32;
+// The current reflector is addressed by absolute row: xa[i] = v_i, and
+// xa[i] = 0 for every retired row (i < s) and padding row (i >= m), so the row
+// loops need no predicates and every lane of a warp takes the same path (the
+// start row depends only on s).
+//   grid mode   : xa = xbuf, refilled from the winner's global slot each step;
+//   cluster mode: xa = the winner's slot in this CTA's own shared memory (every
+//                 CTA pushed its candidate to every other CTA before the barrier).
 
 template <int S, int R, bool kCluster>
 __global__ void __launch_bounds__(max_threads_for<R>())
 cpqr_resident_kernel(ResidentArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int m = a.m, nc = a.nc, l0 = a.l0, lds = a.lds;
+    const int G = gridDim.x;
     const int span = max(m, l0 + R * S);
-    const int xlen = ((kGuard + span + S + 1) + 1) & ~1;
-    const int slot_len = kHdr + ((m + 1) & ~1);
-    double* xbuf = sm;
-    double* xv = xbuf + kGuard;
-    double* rows = xbuf + xlen;                                      // nc * lds
+    const int xlen = (span + S + 1) & ~1;       // absolute reflector rows 0 .. span+S-1
+    const int gslot = kHdr + ((m + 1) & ~1);    // grid slot: header + rows first .. m-1
+    const int cslot = xlen + kCHdr;             // cluster slot: absolute rows, then the header
+    double* xbuf = sm;               // grid: the current reflector; cluster: staging scratch
+    double* xpull = xbuf + xlen;     // cluster pull mode: reflector double buffer (2 x xlen)
+    double* rows = xpull + 2 * xlen;                                 // nc * lds
     double* s_live = rows + static_cast<size_t>(nc) * lds;           // nc
     double* s_anchor = s_live + nc;                                  // nc
     long long* s_pos = reinterpret_cast<long long*>(s_anchor + nc);  // nc (positions < 2^31)
-    double* cslots = reinterpret_cast<double*>(s_pos + nc);          // cluster: [3][slot_len]
+    // cluster slots, 16-B aligned: push mode [3][G][cslot]; pull mode [3][cslot]
+    // (own) followed by the header copies [3][G][kCHdr]
+    double* cslots = reinterpret_cast<double*>(s_pos + nc);
+    cslots += (reinterpret_cast<uintptr_t>(cslots) >> 3) & 1;
+    const bool push = a.push != 0;
+    double* chdr = cslots + 3 * cslot;
 
     __shared__ double red_d[32];
     __shared__ long long red_l[32];
-    __shared__ double s_sc[3];      // tau, beta, scale of the current pivot
-    __shared__ long long s_sel[3];  // pivot column, its position before the swap, winning CTA (-2: tie pass)
-    __shared__ double s_rec[3][2];  // cluster: own records {vmax, pos}
+    __shared__ double s_wv[32];     // per-warp argmax records
+    __shared__ unsigned s_wp[32];
+    __shared__ unsigned s_wl[32];
+    __shared__ double s_sc[3];      // grid: tau, beta, scale of the current pivot
+    __shared__ long long s_sel[3];  // grid: pivot column, its position before the swap, winning CTA (-2: tie pass)
+    __shared__ unsigned long long s_mbar[2];      // cluster: bulk-push barriers, one per slot parity
+    __shared__ double s_rv[kCluster ? 1 : 160];  // grid: the G records of this exchange
+    __shared__ unsigned s_rp[kCluster ? 1 : 160];
 
     const int tid = threadIdx.x, T = blockDim.x;
     const int lane = tid & 31, wid = tid >> 5, nw = T >> 5;
     const int lc = tid / S, q = tid % S;
-    const int G = gridDim.x;
     const int me = kCluster ? static_cast<int>(cg::this_cluster().block_rank()) : blockIdx.x;
     const int64_t c0 = static_cast<int64_t>(me) * nc;
     const int myn = static_cast<int>(max(0LL, min(static_cast<long long>(a.n - c0), static_cast<long long>(nc))));
@@ -192,12 +252,25 @@ cpqr_resident_kernel(ResidentArgs a) {
     const int nsr = l0 / S;  // l0 is a multiple of S
     double* myrows = rows + static_cast<size_t>(lc < nc ? lc : 0) * lds;
     const int gbase = lane & ~(S - 1);
+    constexpr unsigned kFull = 0xffffffffu;
 
-    auto trace = [&](int s, int ph) {
-        if (a.trace != nullptr && tid == 0) a.trace[(static_cast<size_t>(me) * (a.k + 1) + s) * 8 + ph] = globaltimer();
+    auto trace_by = [&](bool who, int s, int ph) {
+        if (a.trace != nullptr && who && s >= 0)
+            a.trace[(static_cast<size_t>(me) * (a.k + 1) + s) * 16 + ph] = globaltimer();
     };
+    auto trace = [&](int s, int ph) { trace_by(tid == 0, s, ph); };
 
-    for (int i = tid; i < xlen; i += T) xbuf[i] = 0.0;
+    for (int i = tid; i < 3 * xlen; i += T) xbuf[i] = 0.0;
+    if constexpr (kCluster) {
+        const int zn = push ? 3 * G * cslot : 3 * cslot + 3 * G * kCHdr;
+        for (int i = tid; i < zn; i += T) cslots[i] = 0.0;
+        if (tid == 0) {
+            mbar_init(smem_u32(&s_mbar[0]), 1);
+            mbar_init(smem_u32(&s_mbar[1]), 1);
+            fence_mbar_init();
+        }
+    }
+    unsigned mbar_phase = 0;  // bit p = phase parity of s_mbar[p]
 
     // ---- load (the only read of W) and initial norms (qr.cpp:56-62) ----
     double yr[R];
@@ -220,6 +293,13 @@ cpqr_resident_kernel(ResidentArgs a) {
         s_anchor[lc] = part;
         s_pos[lc] = col;
     }
+    if constexpr (kCluster) cg::this_cluster().sync();  // slots zeroed before any CTA pushes
+    else __syncthreads();
+
+    // the current pivot (identical in every thread after an exchange)
+    long long piv = 0, ppos = 0;
+    double tau = 0.0, beta = 0.0;
+    const double* xa = xbuf;
 
     // This group's column: alpha = row `first`, tail = sum of squares below it.
     auto partials = [&](int first, double& al, double& tl) {
@@ -243,36 +323,281 @@ cpqr_resident_kernel(ResidentArgs a) {
         tl = group_sum<S>(t0 + t1);
     };
 
-    // CTA argmax (qr.cpp:66-78 over this CTA's columns): the max live norm,
-    // then the lowest position that qualifies against it; 32-bit redux.sync
-    // per warp and one __syncthreads per pass.
-    auto local_max = [&](bool cand, double lv) -> double {
-        const double mx = warp_max_nonneg(cand ? lv : -1.0);
-        if (lane == 0) red_d[wid] = mx;
-        __syncthreads();
-        return warp_max_nonneg(lane < nw ? red_d[lane] : -1.0);
-    };
+    // Exact CTA pick against a given threshold vmax (qr.cpp:66-78 over this
+    // CTA's columns): the lowest position that qualifies; two 32-bit redux.sync
+    // per warp and one __syncthreads.
     auto local_pick = [&](bool cand, double lv, long long pos, double vmax, int& winlc) -> int {
         const unsigned key = (cand && qualifies(lv, vmax)) ? static_cast<unsigned>(pos) : 0xffffffffu;
-        const unsigned wm = __reduce_min_sync(0xffffffffu, key);
-        const unsigned wl = __reduce_min_sync(0xffffffffu, (key == wm) ? static_cast<unsigned>(lc) : 0xffffffffu);
+        const unsigned wm = __reduce_min_sync(kFull, key);
+        const unsigned wl = __reduce_min_sync(kFull, (key == wm) ? static_cast<unsigned>(lc) : 0xffffffffu);
         if (lane == 0) red_l[wid] = static_cast<long long>((static_cast<unsigned long long>(wm) << 32) | wl);
         __syncthreads();
         const unsigned long long mine = lane < nw ? static_cast<unsigned long long>(red_l[lane]) : ~0ull;
-        const unsigned best = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(mine >> 32));
+        const unsigned best = __reduce_min_sync(kFull, static_cast<unsigned>(mine >> 32));
         winlc = static_cast<int>(__reduce_min_sync(
-            0xffffffffu, static_cast<unsigned>(mine >> 32) == best ? static_cast<unsigned>(mine) : 0xffffffffu));
+            kFull, static_cast<unsigned>(mine >> 32) == best ? static_cast<unsigned>(mine) : 0xffffffffu));
         return best == 0xffffffffu ? INT_MAX : static_cast<int>(best);
     };
 
-    auto slot_ptr = [&](int slot, int g) -> double* {
-        if constexpr (kCluster) {
-            double* mineptr = cslots + slot * slot_len;
-            return g == me ? mineptr : cg::this_cluster().map_shared_rank(mineptr, g);
-        } else {
-            return a.slots + (static_cast<size_t>(slot) * G + g) * slot_len;
+    // CTA argmax in one __syncthreads: each warp reduces (max live, lowest
+    // position qualifying against it, its column), then every warp combines
+    // the warp records identically.  A warp whose max qualifies against the CTA
+    // max without equalling it picked against a lower threshold -- ambiguous,
+    // resolved exactly by local_pick (rare: needs norms within 4e-14).
+    auto cta_argmax = [&](bool cand, double lv, long long pos, int& winpos, int& winlc) -> double {
+        const double wm = warp_max_nonneg(cand ? lv : -1.0);
+        const unsigned key = (cand && qualifies(lv, wm)) ? static_cast<unsigned>(pos) : 0xffffffffu;
+        const unsigned wp = __reduce_min_sync(kFull, key);
+        const unsigned wl = __reduce_min_sync(kFull, key == wp ? static_cast<unsigned>(lc) : 0xffffffffu);
+        if (lane == 0) {
+            s_wv[wid] = wm;
+            s_wp[wid] = wp;
+            s_wl[wid] = wl;
+        }
+        __syncthreads();
+        const double v = lane < nw ? s_wv[lane] : -1.0;
+        const unsigned p = lane < nw ? s_wp[lane] : 0xffffffffu;
+        const unsigned l = lane < nw ? s_wl[lane] : 0xffffffffu;
+        const double cmax = warp_max_nonneg(v);
+        const bool qu = v >= 0.0 && qualifies(v, cmax);
+        if (__any_sync(kFull, qu && v != cmax)) {
+            winpos = local_pick(cand, lv, pos, cmax, winlc);
+            return cmax;
+        }
+        const unsigned bp = __reduce_min_sync(kFull, qu ? p : 0xffffffffu);
+        winlc = static_cast<int>(__reduce_min_sync(kFull, (qu && p == bp) ? l : 0xffffffffu));
+        winpos = bp == 0xffffffffu ? INT_MAX : static_cast<int>(bp);
+        return cmax;
+    };
+
+    // Trailing axpy y -= w v of this thread's rows for the current step.  The
+    // norm downdate needs only w, so in cluster mode the axpy is deferred and
+    // runs while the exchange for the next pivot is in flight.
+    bool todo = false;
+    double wpend = 0.0;
+    int psr0 = 0, prr0 = 0;
+    const double* pxa = xbuf;
+    auto do_axpy = [&]() {
+        if (!todo) return;
+        todo = false;
+        const double w = wpend;
+        const double* xr = pxa + (l0 + q);
+        int r = psr0;
+        for (; r + 4 <= nsr; r += 4) {
+            const int i = q + S * r;
+            const double y0 = myrows[i], y1 = myrows[i + S], y2 = myrows[i + 2 * S], y3 = myrows[i + 3 * S];
+            const double v0 = pxa[i], v1 = pxa[i + S], v2 = pxa[i + 2 * S], v3 = pxa[i + 3 * S];
+            myrows[i] = fma(-w, v0, y0);
+            myrows[i + S] = fma(-w, v1, y1);
+            myrows[i + 2 * S] = fma(-w, v2, y2);
+            myrows[i + 3 * S] = fma(-w, v3, y3);
+        }
+        for (; r < nsr; ++r) {
+            const int i = q + S * r;
+            myrows[i] = fma(-w, pxa[i], myrows[i]);
+        }
+        switch (prr0) {
+#define IDK_AXPY_CASE(r)                                         \
+    case r:                                                      \
+        if constexpr (r < R) yr[r] = fma(-w, xr[S * r], yr[r]);  \
+        [[fallthrough]];
+            IDK_REP32(IDK_AXPY_CASE)
+#undef IDK_AXPY_CASE
+            default:
+                break;
         }
     };
+
+    // ---------------- cluster exchange (push, then all-local select) ----------------
+    auto cl_slot = [&](int sl, int g) { return cslots + static_cast<size_t>(sl * G + g) * cslot; };  // push mode
+    auto own_slot = [&](int sl) { return cslots + static_cast<size_t>(push ? sl * G + me : sl) * cslot; };
+    auto hdr_of = [&](int sl, int g) -> double* {
+        return push ? cl_slot(sl, g) + xlen : chdr + static_cast<size_t>(sl * G + g) * kCHdr;
+    };
+
+    // Stage this CTA's candidate in its own slot `sl`: header {col, tau, beta,
+    // scale, vmax, pos} and v by absolute row, zeros on rows [lo, first).
+    auto cl_stage = [&](int sl, double mx, int winpos, int winlc, int first, int lo) {
+        const bool have = winpos != INT_MAX;
+        double* own = own_slot(sl);
+        double* hd = own + xlen;
+        if (have && lc == winlc) {
+            double al, tl;
+            partials(first, al, tl);
+            double tu, be, sc;
+            reflector(al, tl, m - first, tu, be, sc);
+            double* x = own;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int i = l0 + q + S * r;
+                if (i >= first && i < m) x[i] = tu != 0.0 ? (i == first ? 1.0 : mul_rn(yr[r], sc)) : yr[r];
+            }
+            for (int r = first / S; r < nsr; ++r) {
+                const int i = q + S * r;
+                if (i >= first) x[i] = tu != 0.0 ? (i == first ? 1.0 : mul_rn(myrows[i], sc)) : myrows[i];
+            }
+            if (q == 0) {
+                hd[0] = __longlong_as_double(c0 + winlc);
+                hd[1] = tu;
+                hd[2] = be;
+                hd[3] = sc;
+            }
+        }
+        for (int i = lo + tid; i < first; i += T) own[i] = 0.0;  // retired rows read v = 0
+        if (tid == 0) {
+            hd[4] = have ? mx : -1.0;
+            hd[5] = __longlong_as_double(have ? static_cast<long long>(winpos) : 0xffffffffLL);
+        }
+    };
+
+    // Tie slot (rare): plain DSMEM stores of the slot (push mode) or of the
+    // header (pull mode) to every peer, then barrier.cluster.
+    auto cl_push_slow = [&](int sl) {
+        __syncthreads();
+        cg::cluster_group cluster = cg::this_cluster();
+        double* own = own_slot(sl);
+        double* src = push ? own : own + xlen;
+        double* dst = push ? own : hdr_of(sl, me);
+        const int len = push ? cslot : kCHdr;
+        if (!push && tid < kCHdr) dst[tid] = src[tid];
+        const int tot = (G - 1) * len;
+        for (int e = tid; e < tot; e += T) {
+            const int gi = e / len, j = e - gi * len;
+            const int g = gi < me ? gi : gi + 1;
+            cluster.map_shared_rank(dst, g)[j] = src[j];
+        }
+        cluster.sync();
+    };
+
+    // Every warp reduces the G slot headers of `sl` from local shared memory
+    // (identical result everywhere, no CTA barrier): winning CTA, its position.
+    auto cl_select = [&](int sl, bool& amb, double& gmax, unsigned& bp) -> int {
+        const double* h = hdr_of(sl, lane < G ? lane : 0);
+        const double v = lane < G ? h[4] : -1.0;
+        const unsigned p = lane < G ? static_cast<unsigned>(__double_as_longlong(h[5])) : 0xffffffffu;
+        gmax = warp_max_nonneg(v);
+        const bool qu = v >= 0.0 && qualifies(v, gmax);
+        amb = __any_sync(kFull, qu && v != gmax);
+        bp = __reduce_min_sync(kFull, qu ? p : 0xffffffffu);
+        return static_cast<int>(__reduce_min_sync(kFull, (qu && p == bp) ? static_cast<unsigned>(lane) : 0xffffffffu));
+    };
+
+    // One cluster exchange, for the pivot of step `first`.  The winner group
+    // of each CTA finishes its own column's update, stages it and pushes it
+    // (warp-level ordering only); every other thread finishes its deferred
+    // trailing update meanwhile, so that work overlaps the exchange.
+    auto cluster_round = [&](int first, bool cand, double lv, long long pos, int step) {
+        int winpos, winlc;
+        const double mx = cta_argmax(cand, lv, pos, winpos, winlc);
+        trace(step, 2);
+        int sl = first & 1;
+        const bool have = winpos != INT_MAX;
+        const unsigned mb = smem_u32(&s_mbar[sl]);
+        // The warp holding the winner column builds the next reflector with all
+        // 32 lanes (its deferred update applied on the fly to a raw copy), so
+        // the serial path is a few rows per lane, not the group's whole column.
+        const bool pubwarp = wid == (have ? (winlc * S) >> 5 : 0);
+        if (pubwarp) {
+            double* own = own_slot(sl);
+            double* hd = own + xlen;
+            const int lo = max(0, first - 2) & ~1;
+            const unsigned bytes = push ? static_cast<unsigned>(xlen + kCHdr - lo) * sizeof(double)
+                                        : static_cast<unsigned>(kCHdr * sizeof(double));
+            if (have) {
+                const int wl0 = (winlc * S) & 31;
+                const double ww = __shfl_sync(kFull, todo ? wpend : 0.0, wl0);  // 0: already current
+                if (lc == winlc) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int i = l0 + q + S * r;
+                        if (i >= first && i < m) xbuf[i] = yr[r];
+                    }
+                }
+                __syncwarp();
+                const double* wrow = rows + static_cast<size_t>(winlc) * lds;
+                double al = 0.0, tl = 0.0;
+                for (int i = first + lane; i < m; i += 32) {
+                    const double y = fma(-ww, xa[i], i < l0 ? wrow[i] : xbuf[i]);  // == the group's own axpy
+                    xbuf[i] = y;
+                    if (i == first) al = y;
+                    else tl = fma(y, y, tl);
+                }
+                al = __shfl_sync(kFull, al, first & 31);  // row `first` lives in lane first % 32
+                tl = warp_sum(tl);
+                double tu, be, sc;
+                reflector(al, tl, m - first, tu, be, sc);
+                for (int i = first + lane; i < m; i += 32)
+                    own[i] = tu != 0.0 ? (i == first ? 1.0 : mul_rn(xbuf[i], sc)) : xbuf[i];
+                if (lane == 0) {
+                    hd[0] = __longlong_as_double(c0 + winlc);
+                    hd[1] = tu;
+                    hd[2] = be;
+                    hd[3] = sc;
+                }
+            }
+            if (lane == 0) {
+                for (int i = lo; i < first; ++i) own[i] = 0.0;  // retired rows read v = 0
+                hd[4] = have ? mx : -1.0;
+                hd[5] = __longlong_as_double(have ? static_cast<long long>(winpos) : 0xffffffffLL);
+                if (!push) {
+                    double* mine = hdr_of(sl, me);
+                    for (int j = 0; j < kCHdr; ++j) mine[j] = hd[j];
+                }
+            }
+            fence_proxy_async_smem();  // staging writes (generic proxy) -> bulk-copy reads (async proxy)
+            __syncwarp();
+            // the arrive releases the local staging to this CTA's waiters; the
+            // peers' copies complete the transaction count
+            if (lane == 0) mbar_expect_tx(mb, static_cast<unsigned>(G - 1) * bytes);
+            if (lane < G - 1) {
+                const int g = lane < me ? lane : lane + 1;
+                const unsigned sa = smem_u32(push ? own + lo : hd);
+                const unsigned da = push ? sa : smem_u32(hdr_of(sl, me));
+                bulk_push(mapa_u32(da, g), sa, bytes, mapa_u32(mb, g));
+            }
+            trace_by(lane == 0, step, 3);
+            // let the other warps go: their axpys contend for shared memory, so
+            // they wait until the candidate is out (named barrier 1)
+            asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
+        } else {
+            asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+        }
+        do_axpy();
+        trace(step, 7);
+        mbar_wait(mb, (mbar_phase >> sl) & 1u);
+        mbar_phase ^= 1u << sl;
+        trace(step, 4);
+        bool amb;
+        double gmax;
+        unsigned bp;
+        int gw = cl_select(sl, amb, gmax, bp);
+        if (amb) {
+            // exact tie pass: lowest position with sqrt(live) >= the global threshold
+            const int wp2 = local_pick(cand, lv, pos, gmax, winlc);
+            sl = 2;
+            cl_stage(2, 0.0, wp2, winlc, first, 0);
+            cl_push_slow(2);
+            gw = cl_select(2, amb, gmax, bp);
+        }
+        const double* h = hdr_of(sl, gw);
+        piv = __double_as_longlong(h[0]);
+        tau = h[1];
+        beta = h[2];
+        ppos = bp;
+        if (push) {
+            xa = cl_slot(sl, gw);
+        } else {  // pull the winner's rows over DSMEM into the reflector buffer of this parity
+            const double* src = cg::this_cluster().map_shared_rank(own_slot(sl), gw);
+            double* xb = xpull + (first & 1) * xlen;
+            for (int i = tid; i < xlen; i += T) xb[i] = (i >= first && i < m) ? src[i] : 0.0;
+            __syncthreads();
+            xa = xb;
+        }
+        trace(step, 5);
+    };
+
+    // ---------------- grid exchange (tagged records in L2) ----------------
+    auto slot_ptr = [&](int slot, int g) -> double* { return a.slots + (static_cast<size_t>(slot) * G + g) * gslot; };
 
     // Publish this CTA's candidate (local index winlc, position winpos) for the
     // exchange `tag` in `slot`: header + rows first..m-1, then the record.
@@ -282,8 +607,8 @@ cpqr_resident_kernel(ResidentArgs a) {
         if (have && lc == winlc) {
             double al, tl;
             partials(first, al, tl);
-            double tau, beta, scale;
-            reflector(al, tl, m - first, tau, beta, scale);
+            double tu, be, sc;
+            reflector(al, tl, m - first, tu, be, sc);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int i = l0 + q + S * r;
@@ -291,9 +616,9 @@ cpqr_resident_kernel(ResidentArgs a) {
             }
             if (q == 0) {
                 dst[0] = __longlong_as_double(c0 + winlc);
-                dst[1] = tau;
-                dst[2] = beta;
-                dst[3] = scale;
+                dst[1] = tu;
+                dst[2] = be;
+                dst[3] = sc;
             }
         }
         if (have) {  // shared-memory rows of the candidate, copied by everyone
@@ -303,64 +628,59 @@ cpqr_resident_kernel(ResidentArgs a) {
         __syncthreads();
         if (tid == 0) {
             const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
-            if constexpr (kCluster) {
-                s_rec[slot][0] = mx;
-                s_rec[slot][1] = __longlong_as_double(static_cast<long long>(pos32));
-            } else {
-                __threadfence();  // slot data before the tagged record (release)
-                const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
-                unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * kRecWords;
-                st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
-                st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
-            }
+            __threadfence();  // slot data before the tagged record (release)
+            const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
+            unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * kRecWords;
+            st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
+            st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
         }
     };
 
-    // Record of CTA g for exchange `tag`: {vmax, pos}; grid mode spins until
-    // all three words carry the tag.
+    // Record of CTA g for exchange `tag`: {vmax, pos}; spins until all three
+    // words carry the tag.
     auto read_rec = [&](int slot, int g, unsigned tag, double& vmax, unsigned& pos) {
-        if constexpr (kCluster) {
-            const double* rp = cg::this_cluster().map_shared_rank(&s_rec[slot][0], g);
-            vmax = rp[0];
-            pos = static_cast<unsigned>(__double_as_longlong(rp[1]));
-        } else {
-            const unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + g) * kRecWords;
-            unsigned long long x0, x1, x2, x3;
-            for (;;) {
-                ld_relaxed_v2(rp, x0, x1);
-                ld_relaxed_v2(rp + 2, x2, x3);
-                if (static_cast<unsigned>(x0) == tag && static_cast<unsigned>(x1) == tag &&
-                    static_cast<unsigned>(x2) == tag)
-                    break;
-            }
-            vmax = __longlong_as_double(static_cast<long long>(((x0 >> 32) << 32) | (x1 >> 32)));
-            pos = static_cast<unsigned>(x2 >> 32);
+        const unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + g) * kRecWords;
+        unsigned long long x0, x1, x2, x3;
+        for (;;) {
+            ld_relaxed_v2(rp, x0, x1);
+            ld_relaxed_v2(rp + 2, x2, x3);
+            if (static_cast<unsigned>(x0) == tag && static_cast<unsigned>(x1) == tag && static_cast<unsigned>(x2) == tag)
+                break;
         }
+        vmax = __longlong_as_double(static_cast<long long>(((x0 >> 32) << 32) | (x1 >> 32)));
+        pos = static_cast<unsigned>(x2 >> 32);
     };
 
-    constexpr int kRecPerLane = kCluster ? 1 : 5;  // G <= 32 (cluster) or <= 160 (grid)
+    constexpr int kRecPerLane = 5;  // G <= 160
 
     // Wait for every CTA's record of exchange `tag`, reduce them (identical in
     // every CTA), then copy the winner's column -- scaled by its reflector --
-    // into xv.  `first` = the step the new pivot is for.
+    // into xbuf.  `first` = the step the new pivot is for.
     unsigned epoch = 0;
-    auto exchange = [&](int parity, unsigned tag, int first) {
-        if constexpr (kCluster) cg::this_cluster().sync();
-        if constexpr (!kCluster) {
-            if (a.barrier != nullptr) grid_barrier(a.barrier, epoch);
-        }
+    auto grid_exchange = [&](int parity, unsigned tag, int first, bool cand, double lv, long long pos, int step) {
+        if (a.barrier != nullptr) grid_barrier(a.barrier, epoch);
         int slot = parity;
+        // every thread polls at most a few records, all in flight at once:
+        // one L2 round trip after the last arrival instead of one per record
+        for (int g = tid; g < G; g += T) {
+            double vv;
+            unsigned pp;
+            read_rec(parity, g, tag, vv, pp);
+            s_rv[g] = vv;
+            s_rp[g] = pp;
+        }
+        if (tid < G) __threadfence();  // acquire: slot data after the records
+        __syncthreads();
+        trace(step, 4);
         if (wid == 0) {
             double v[kRecPerLane];
             unsigned p[kRecPerLane];
 #pragma unroll
             for (int t = 0; t < kRecPerLane; ++t) {
                 const int g = lane + 32 * t;
-                v[t] = -1.0;
-                p[t] = 0xffffffffu;
-                if (g < G) read_rec(parity, g, tag, v[t], p[t]);
+                v[t] = g < G ? s_rv[g] : -1.0;
+                p[t] = g < G ? s_rp[g] : 0xffffffffu;
             }
-            if constexpr (!kCluster) __threadfence();  // acquire: slot data after the records
             double vmax = -1.0;
 #pragma unroll
             for (int t = 0; t < kRecPerLane; ++t) vmax = fmax(vmax, v[t]);
@@ -377,8 +697,8 @@ cpqr_resident_kernel(ResidentArgs a) {
                     }
                 }
             }
-            amb = __any_sync(0xffffffffu, amb);
-            const unsigned wb = __reduce_min_sync(0xffffffffu, best);
+            amb = __any_sync(kFull, amb);
+            const unsigned wb = __reduce_min_sync(kFull, best);
             if (best == wb && best != 0xffffffffu) {  // unique lane: positions are distinct
                 s_sel[0] = amb ? -2 : 0;
                 s_sel[1] = wb;
@@ -387,14 +707,13 @@ cpqr_resident_kernel(ResidentArgs a) {
             if (lane == 0) red_d[0] = vmax;
         }
         __syncthreads();
+        trace(step, 5);
         if (s_sel[0] == -2) {
             // Exact tie pass: lowest position with sqrt(live) >= the global threshold.
             const double vmax = red_d[0];
-            const bool cand = active && q == 0 && s_pos[lc] >= first;
             int winlc;
-            const int winpos = local_pick(cand, cand ? s_live[lc] : -1.0, cand ? s_pos[lc] : 0, vmax, winlc);
+            const int winpos = local_pick(cand, lv, pos, vmax, winlc);
             publish(2, tag, 0.0, winpos, winlc, first);
-            if constexpr (kCluster) cg::this_cluster().sync();
             slot = 2;
             if (wid == 0) {
                 unsigned b2 = 0xffffffffu;
@@ -408,8 +727,8 @@ cpqr_resident_kernel(ResidentArgs a) {
                         g2 = g;
                     }
                 }
-                if constexpr (!kCluster) __threadfence();
-                const unsigned wb = __reduce_min_sync(0xffffffffu, b2);
+                __threadfence();
+                const unsigned wb = __reduce_min_sync(kFull, b2);
                 if (b2 == wb && b2 != 0xffffffffu) {
                     s_sel[0] = 0;
                     s_sel[1] = wb;
@@ -418,42 +737,48 @@ cpqr_resident_kernel(ResidentArgs a) {
             }
             __syncthreads();
         }
-        // All threads: header + winner's column (one round trip), scaled into xv.
+        // All threads: header + winner's column (one round trip), scaled into xbuf by absolute row.
         const double* src = slot_ptr(slot, static_cast<int>(s_sel[2]));
-        const int len = m - first;
-        const double h0 = kCluster ? src[0] : __ldcg(src);
-        const double tau = kCluster ? src[1] : __ldcg(src + 1);
-        const double beta = kCluster ? src[2] : __ldcg(src + 2);
-        const double scale = kCluster ? src[3] : __ldcg(src + 3);
-        for (int i = tid; i < len; i += T) {
-            const double x = kCluster ? src[kHdr + i] : __ldcg(src + kHdr + i);
-            xv[i] = tau != 0.0 ? (i == 0 ? 1.0 : mul_rn(x, scale)) : x;
+        const double h0 = __ldcg(src);
+        const double tu = __ldcg(src + 1);
+        const double be = __ldcg(src + 2);
+        const double sc = __ldcg(src + 3);
+        for (int i = tid; i < xlen; i += T) {
+            double x = 0.0;
+            if (i >= first && i < m) {
+                x = __ldcg(src + kHdr + i - first);
+                if (tu != 0.0) x = i == first ? 1.0 : mul_rn(x, sc);
+            }
+            xbuf[i] = x;
         }
-        for (int i = len + tid; i < span + S; i += T) xv[i] = 0.0;  // stale tail of the previous pivot
-        if (tid == 0) {
-            s_sel[0] = __double_as_longlong(h0);
-            s_sc[0] = tau;
-            s_sc[1] = beta;
-            s_sc[2] = scale;
-        }
+        const long long sel1 = s_sel[1];
         __syncthreads();
+        piv = __double_as_longlong(h0);
+        ppos = sel1;
+        tau = tu;
+        beta = be;
+        xa = xbuf;
+    };
+
+    auto grid_round = [&](int first, bool cand, double lv, long long pos, int step) {
+        int winpos, winlc;
+        const double mx = cta_argmax(cand, lv, pos, winpos, winlc);
+        trace(step, 2);
+        const int parity = first & 1;
+        publish(parity, static_cast<unsigned>(first + 1), mx, winpos, winlc, first);
+        trace(step, 3);
+        grid_exchange(parity, static_cast<unsigned>(first + 1), first, cand, lv, pos, step);
     };
 
     // ---- pivot 0 ----
     {
-        __syncthreads();
         const bool cand = active && q == 0;
         const double lv = cand ? s_live[lc] : -1.0;
-        const double mx = local_max(cand, lv);
-        int winlc;
-        const int winpos = local_pick(cand, lv, cand ? s_pos[lc] : 0, mx, winlc);
-        publish(0, 1u, mx, winpos, winlc, 0);
-        exchange(0, 1u, 0);
+        if constexpr (kCluster) cluster_round(0, cand, lv, cand ? s_pos[lc] : 0, -1);
+        else grid_round(0, cand, lv, cand ? s_pos[lc] : 0, -1);
     }
 
     for (int s = 0; s < a.k; ++s) {
-        const long long piv = s_sel[0], ppos = s_sel[1];
-        const double tau = s_sc[0];
         trace(s, 0);
         if (me == 0 && tid == 0) {
             a.taus[s] = tau;
@@ -462,31 +787,34 @@ cpqr_resident_kernel(ResidentArgs a) {
         // Replay the swap on positions (qr.cpp:79-86); the group leader owns
         // its column's position, every member keeps a copy.
         long long mypos = -1;
+        double live0 = 0.0, anchor0 = 0.0;
         if (active) {
             mypos = s_pos[lc];
+            live0 = s_live[lc];
+            anchor0 = s_anchor[lc];
             if (col == piv) mypos = s;
             else if (mypos == s) mypos = ppos;
-            if (q == 0) s_pos[lc] = mypos;
         }
+        __syncwarp();
+        if (active && q == 0) s_pos[lc] = mypos;
 
         // ---- trailing update + downdate (qr.cpp:93-106) ----
         const int dreg = s - l0;
         const int rr0 = dreg <= 0 ? 0 : dreg / S;
         const int sr0 = s / S;
-        const double* xr = xv + (l0 + q - s);  // xr[S*r] = v for register row r
+        const double* xr = xa + (l0 + q);  // xr[S*r] = v for register row r
         bool cand = false;
         double lv = -1.0;
         if (active && col == piv) {
             if (tau != 0.0) {  // the pivot column becomes [R; beta; v] like the reference's work
-                const double beta = s_sc[1];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const int i = l0 + q + S * r;
-                    if (i >= s && i < m) yr[r] = (i == s) ? beta : xv[i - s];
+                    if (i >= s && i < m) yr[r] = (i == s) ? beta : xa[i];
                 }
                 for (int r = sr0; r < nsr; ++r) {
                     const int i = q + S * r;
-                    if (i >= s) myrows[i] = (i == s) ? beta : xv[i - s];
+                    if (i >= s) myrows[i] = (i == s) ? beta : xa[i];
                 }
             }
         } else if (mypos > s) {
@@ -516,7 +844,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                 for (; r + 4 <= nsr; r += 4) {
                     const int i = q + S * r;
                     const double y0 = myrows[i], y1 = myrows[i + S], y2 = myrows[i + 2 * S], y3 = myrows[i + 3 * S];
-                    const double v0 = xv[i - s], v1 = xv[i - s + S], v2 = xv[i - s + 2 * S], v3 = xv[i - s + 3 * S];
+                    const double v0 = xa[i], v1 = xa[i + S], v2 = xa[i + 2 * S], v3 = xa[i + 3 * S];
                     d0 = fma(v0, y0, d0);
                     d1 = fma(v1, y1, d1);
                     d2 = fma(v2, y2, d2);
@@ -524,7 +852,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                 }
                 for (; r < nsr; ++r) {
                     const int i = q + S * r;
-                    d0 = fma(xv[i - s], myrows[i], d0);
+                    d0 = fma(xa[i], myrows[i], d0);
                 }
                 switch (rr0) {
 #define IDK_DOT_CASE(r)                                                     \
@@ -542,36 +870,18 @@ cpqr_resident_kernel(ResidentArgs a) {
                         break;
                 }
                 const double w = mul_rn(group_sum<S>((d0 + d1) + (d2 + d3)), tau);
-                r = sr0;
-                for (; r + 4 <= nsr; r += 4) {
-                    const int i = q + S * r;
-                    const double y0 = myrows[i], y1 = myrows[i + S], y2 = myrows[i + 2 * S], y3 = myrows[i + 3 * S];
-                    const double v0 = xv[i - s], v1 = xv[i - s + S], v2 = xv[i - s + 2 * S], v3 = xv[i - s + 3 * S];
-                    myrows[i] = fma(-w, v0, y0);
-                    myrows[i + S] = fma(-w, v1, y1);
-                    myrows[i + 2 * S] = fma(-w, v2, y2);
-                    myrows[i + 3 * S] = fma(-w, v3, y3);
-                }
-                for (; r < nsr; ++r) {
-                    const int i = q + S * r;
-                    myrows[i] = fma(-w, xv[i - s], myrows[i]);
-                }
-                switch (rr0) {
-#define IDK_AXPY_CASE(r)                                         \
-    case r:                                                      \
-        if constexpr (r < R) yr[r] = fma(-w, xr[S * r], yr[r]);  \
-        [[fallthrough]];
-                    IDK_REP32(IDK_AXPY_CASE)
-#undef IDK_AXPY_CASE
-                    default:
-                        break;
-                }
+                wpend = w;
+                psr0 = sr0;
+                prr0 = rr0;
+                pxa = xa;
+                todo = true;
                 head = ys - w;  // row s has v_0 = 1
             }
-            lv = sub_rn(s_live[lc], mul_rn(head, head));
+            lv = sub_rn(live0, mul_rn(head, head));
             if (lv < 0.0) lv = 0.0;
-            if (lv <= mul_rn(kRecomp, s_anchor[lc])) {
-                // fresh = sum_{i > s} y_i^2 (qr.cpp:101-104)
+            if (lv <= mul_rn(kRecomp, anchor0)) {
+                // fresh = sum_{i > s} y_i^2 (qr.cpp:101-104) of the updated column
+                do_axpy();
                 double al, tl;
                 partials(s + 1, al, tl);
                 lv = fma(al, al, tl);
@@ -579,19 +889,17 @@ cpqr_resident_kernel(ResidentArgs a) {
             }
             if (q == 0) s_live[lc] = lv;
             cand = q == 0;
+            if constexpr (!kCluster) do_axpy();
         }
         trace(s, 1);
-        if (s + 1 == a.k) break;
+        if (s + 1 == a.k) {
+            do_axpy();
+            break;
+        }
 
         // ---- next pivot: CTA candidate, exchange ----
-        const int parity = (s + 1) & 1;
-        const double mx = local_max(cand, lv);
-        int winlc;
-        const int winpos = local_pick(cand, lv, mypos, mx, winlc);
-        trace(s, 2);
-        publish(parity, static_cast<unsigned>(s + 2), mx, winpos, winlc, s + 1);
-        trace(s, 3);
-        exchange(parity, static_cast<unsigned>(s + 2), s + 1);
+        if constexpr (kCluster) cluster_round(s + 1, cand, lv, mypos, s);
+        else grid_round(s + 1, cand, lv, mypos, s);
         trace(s, 6);
     }
 
@@ -609,7 +917,7 @@ cpqr_resident_kernel(ResidentArgs a) {
         }
         if (q == 0) a.pos_out[col] = s_pos[lc];
     }
-    if constexpr (kCluster) cg::this_cluster().sync();  // keep shared memory alive for DSMEM readers
+    if constexpr (kCluster) cg::this_cluster().sync();  // keep shared memory alive for DSMEM pushes
 }
 
 // ------------------------------------------------------------------------------------
@@ -626,16 +934,16 @@ int pad_lds(int l0, int S) {
     return lds;
 }
 
-size_t resident_smem(int m, int nc, int l0, int lds, int S, int R, bool cluster) {
-    const size_t slot_len = kHdr + static_cast<size_t>((m + 1) & ~1);
+size_t resident_smem(int m, int nc, int l0, int lds, int S, int R, bool cluster, int G, bool push) {
     const int span = std::max(m, l0 + R * S);
-    const size_t xlen = static_cast<size_t>(((kGuard + span + S + 1) + 1) & ~1);
-    size_t d = xlen + static_cast<size_t>(nc) * lds + 2 * static_cast<size_t>(nc) + static_cast<size_t>(nc);
-    if (cluster) d += 3 * slot_len;
+    const size_t xlen = static_cast<size_t>((span + S + 1) & ~1);
+    size_t d = 3 * xlen + static_cast<size_t>(nc) * lds + 2 * static_cast<size_t>(nc) + static_cast<size_t>(nc);
+    if (cluster)  // + alignment pad
+        d += (push ? 3 * static_cast<size_t>(G) * (kCHdr + xlen) : 3 * (kCHdr + xlen) + 3 * static_cast<size_t>(G) * kCHdr) + 2;
     return d * sizeof(double);
 }
 
-ResidentPlan plan_for(int m, int64_t n, int k, int G_target, bool cluster, size_t smem_cap) {
+ResidentPlan plan_for(int m, int64_t n, int k, int G_target, bool cluster, size_t smem_cap, bool push) {
     ResidentPlan best;
     int64_t G = std::min<int64_t>(n, G_target);
     const int nc = static_cast<int>((n + G - 1) / G);
@@ -653,7 +961,7 @@ ResidentPlan plan_for(int m, int64_t n, int k, int G_target, bool cluster, size_
             int l0 = std::max(0, m - reg_rows);
             l0 = ((l0 + S - 1) / S) * S;  // uniform loop bounds need S | l0
             const int lds = pad_lds(l0, S);
-            const size_t smem = resident_smem(m, nc, l0, lds, S, R, cluster);
+            const size_t smem = resident_smem(m, nc, l0, lds, S, R, cluster, static_cast<int>(G), push);
             if (smem > smem_cap) continue;
             // cost model: per-step serial work of one thread (register rows are
             // cheap, shared rows cost ~3 LDS/STS each) -- the step latency --
@@ -662,6 +970,7 @@ ResidentPlan plan_for(int m, int64_t n, int k, int G_target, bool cluster, size_
             if (!best.ok || cost < best.cost) {
                 best.ok = true;
                 best.cluster = cluster;
+                best.push = cluster && push;
                 best.G = static_cast<int>(G);
                 best.nc = nc;
                 best.S = S;
@@ -696,10 +1005,12 @@ void* pick_kernel(int S, int R) {
 
 // Plan the on-chip CPQR of an m x n matrix: a single cluster (<= 16 CTAs,
 // DSMEM exchange) when it fits, else one CTA per SM with the grid exchange.
-ResidentPlan cpqr_resident_plan(int m, int64_t n, int k, int num_sms, bool allow_cluster) {
+ResidentPlan cpqr_resident_plan(int m, int64_t n, int k, int num_sms, int cluster_pref) {
     const size_t cap = 200 * 1024;
-    if (allow_cluster && n >= 32) {
-        ResidentPlan p = plan_for(m, n, k, 16, true, cap);
+    if (cluster_pref != 1 && n >= 32) {
+        ResidentPlan p;
+        if (cluster_pref == 0) p = plan_for(m, n, k, 16, true, cap, true);
+        if (!p.ok) p = plan_for(m, n, k, 16, true, cap, false);
         if (p.ok) {
             void* fn = pick_kernel<true>(p.S, p.R);
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
@@ -719,8 +1030,9 @@ ResidentPlan cpqr_resident_plan(int m, int64_t n, int k, int num_sms, bool allow
             if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) == cudaSuccess && clusters >= 1) return p;
             cudaGetLastError();
         }
+        if (cluster_pref == 2) return ResidentPlan();
     }
-    return plan_for(m, n, k, num_sms, false, cap);
+    return plan_for(m, n, k, num_sms, false, cap, false);
 }
 
 long long* g_trace = nullptr;  // debug: set by idk_debug_cpqr_trace
@@ -754,6 +1066,7 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     a.rec = reinterpret_cast<unsigned long long*>(e);
     a.slots = reinterpret_cast<double*>(e + sizeof(unsigned long long) * kRecWords * 3 * G);
     a.trace = g_trace;
+    a.push = p.push ? 1 : 0;
     void* args[] = {&a};
     if (p.cluster) {
         void* fn = pick_kernel<true>(p.S, p.R);

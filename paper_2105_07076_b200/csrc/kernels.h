@@ -35,11 +35,13 @@ cudaError_t cpqr_finish(const double* W, int64_t ldw, int m, int64_t n, int k, c
 struct ResidentPlan {
     bool ok = false;
     bool cluster = false;
+    bool push = false;  // cluster exchange: every CTA holds every candidate column
     int G = 0, nc = 0, S = 0, R = 0, l0 = 0, lds = 0, threads = 0;
     size_t smem = 0;
     double cost = 0;
 };
-ResidentPlan cpqr_resident_plan(int m, int64_t n, int k, int num_sms, bool allow_cluster);
+// cluster_pref: 0 = cluster (push, else pull) when it fits, else grid; 1 = grid only; 2 = cluster pull only
+ResidentPlan cpqr_resident_plan(int m, int64_t n, int k, int num_sms, int cluster_pref);
 void cpqr_resident_set_trace(long long* device_buf);  // debug phase timing (nullptr = off)
 size_t cpqr_resident_exchange_bytes(const ResidentPlan& p, int m);
 cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, int m, int64_t n, int k,

@@ -115,7 +115,7 @@ class Context:
         return int(self.lib.idk_kernel_launches(self.h))
 
     STAGES = ("prep", "sketch", "cpqr", "solve", "gather")
-    CPQR_AUTO, CPQR_RESIDENT_GRID, CPQR_STREAMING = 0, 1, 2
+    CPQR_AUTO, CPQR_RESIDENT_GRID, CPQR_STREAMING, CPQR_CLUSTER_PULL = 0, 1, 2, 3
 
     def set_cpqr_mode(self, mode: int):
         self.check(self.lib.idk_set_cpqr_mode(self.h, mode))
@@ -126,7 +126,7 @@ class Context:
     def cpqr_plan(self, m: int, n: int, k: int) -> dict:
         out = (C.c_int64 * 8)()
         self.check(self.lib.idk_cpqr_plan(self.h, m, n, k, out))
-        kinds = {1: "cluster", 2: "resident-grid", 3: "streaming"}
+        kinds = {1: "cluster", 2: "resident-grid", 3: "streaming", 4: "cluster-pull"}
         keys = ("kind", "ctas", "cols_per_cta", "threads_per_col", "reg_rows", "smem_rows", "threads", "smem")
         d = dict(zip(keys, list(out)))
         d["kind"] = kinds[d["kind"]]

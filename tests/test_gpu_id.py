@@ -32,7 +32,8 @@ def idk():
     return idk
 
 
-@pytest.fixture(autouse=True, params=[0, 1, 2], ids=["cpqr-auto", "cpqr-resident-grid", "cpqr-streaming"])
+@pytest.fixture(autouse=True, params=[0, 1, 2, 3],
+                ids=["cpqr-auto", "cpqr-resident-grid", "cpqr-streaming", "cpqr-cluster-pull"])
 def cpqr_mode(request, idk):
     """Every case runs on each CPQR kernel: cluster/resident (auto), resident grid, streaming."""
     ctx = idk.context(0)

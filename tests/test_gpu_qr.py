@@ -27,7 +27,8 @@ def idk():
     return idk
 
 
-@pytest.fixture(autouse=True, params=[0, 1, 2], ids=["cpqr-auto", "cpqr-resident-grid", "cpqr-streaming"])
+@pytest.fixture(autouse=True, params=[0, 1, 2, 3],
+                ids=["cpqr-auto", "cpqr-resident-grid", "cpqr-streaming", "cpqr-cluster-pull"])
 def cpqr_mode(request, idk):
     """Every case runs on each CPQR kernel: cluster/resident (auto), resident grid, streaming."""
     ctx = idk.context(0)
@@ -162,7 +163,7 @@ def test_planner_picks_on_chip_kernels(idk, cpqr_mode):
     if cpqr_mode != 0:
         pytest.skip("plan check runs once")
     assert ctx.cpqr_plan(110, 4000, 100)["kind"] == "cluster"      # cfg2 sketch
-    assert ctx.cpqr_plan(500, 1000, 50)["kind"] == "cluster"       # cfg1
+    assert ctx.cpqr_plan(500, 1000, 50)["kind"] == "cluster-pull"  # cfg1: slots of 500 rows x 16 CTAs do not fit
     assert ctx.cpqr_plan(272, 16384, 256)["kind"] == "resident-grid"  # cfg4 sketch
     assert ctx.cpqr_plan(72, 65536, 64)["kind"] == "resident-grid"    # cfg5 sketch
 

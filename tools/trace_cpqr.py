@@ -1,5 +1,10 @@
 """Per-phase breakdown of the resident CPQR kernel from %globaltimer marks of
-every CTA: python tools/trace_cpqr.py cfg2 [mode]"""
+every CTA: python tools/trace_cpqr.py cfg2 [mode]
+
+Marks per step s: 0 top, 1 trailing update (cluster: dot + downdate) done,
+2 CTA argmax done, 3 candidate + record published (cluster: by the publishing
+warp), 4 all records read (after the barrier / polling), 5 winner selected,
+6 reflector in place (= next step's top), 7 cluster: tid 0's deferred axpy done."""
 import ctypes as C
 import os
 import sys
@@ -21,7 +26,7 @@ mm = cfg.l if cfg.randomized else min(cfg.m, cfg.n)
 nn = max(cfg.m, cfg.n) if cfg.randomized else cfg.n
 plan = ctx.cpqr_plan(mm, nn, cfg.k)
 G, k = plan["ctas"], cfg.k
-buf = torch.zeros(G * (k + 1) * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(G * (k + 1) * 16, dtype=torch.int64, device="cuda")
 for it in range(3):
     ctx.lib.idk_debug_cpqr_trace(ctx.h, C.c_void_p(buf.data_ptr()) if it == 2 else None)
     if cfg.randomized:
@@ -29,28 +34,27 @@ for it in range(3):
     else:
         idk.id_auto(a, cfg.k, idk.DETERMINISTIC)
 ctx.lib.idk_debug_cpqr_trace(ctx.h, None)
-t = buf.cpu().numpy().reshape(G, k + 1, 8).astype(np.float64)[:, :k, :]
+t = buf.cpu().numpy().reshape(G, k + 1, 16).astype(np.float64)[:, :k, :]
 steps = k - 1
-names = ["update", "local argmax", "push cand+rec", "(unused)", "barrier", "select+copy", "->next top"]
 print(name, "mode", mode, "plan", plan)
-print(f"{'phase':20s} {'cta0 ns':>9s} {'mean ns':>9s} {'max ns':>9s}")
+print(f"{'phase':24s} {'cta0 ns':>9s} {'mean ns':>9s} {'max ns':>9s}")
+names = ["trailing update", "CTA argmax", "publish cand+record", "wait + read records", "select (CTA sync)",
+         "copy winner column"]
 for i, nm in enumerate(names):
-    if i == 3:
-        continue
-    if i == 4:
-        d = t[:, :steps, 5] - t[:, :steps, 3]
-    elif i < 6:
-        d = t[:, :steps, i + 1] - t[:, :steps, i]
-    else:
-        d = t[:, 1:steps + 1, 0] - t[:, :steps, 6]
-    print(f"{nm:20s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
-for nm, (x, y) in [("  records loaded", (5, 4)), ("  reduce+sync", (4, 7)), ("  column copy", (7, 6))]:
-    d = t[:, :steps, y] - t[:, :steps, x]
-    print(f"{nm:20s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+    d = t[:, :steps, i + 1] - t[:, :steps, i]
+    print(f"{nm:24s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+d = t[:, 1:steps + 1, 0] - t[:, :steps, 6]
+print(f"{'-> next top':24s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
 arr = t[:, :steps, 3]
 print(f"arrival skew (max-min over CTAs of 'record written'): {(arr.max(0) - arr.min(0)).mean():.0f} ns")
-rel = t[:, :steps, 5]
-print(f"release skew (max-min of 'barrier done'): {(rel.max(0) - rel.min(0)).mean():.0f} ns; "
+rel = t[:, :steps, 4]
+print(f"release skew (max-min of 'records read'): {(rel.max(0) - rel.min(0)).mean():.0f} ns; "
       f"last arrival -> first release: {(rel.min(0) - t[:, :steps, 3].max(0)).mean():.0f} ns")
 tot = (t[0, 1:steps + 1, 0] - t[0, :steps, 0])
 print(f"step (cta0): mean {tot.mean():.0f} ns  first {tot[0]:.0f}  last {tot[-1]:.0f}")
+if t[:, :steps, 7].max() > 0:
+    d = t[:, :steps, 7] - t[:, :steps, 2]
+    print(f"{'(tid0 deferred axpy)':24s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+for lo, hi in [(0, 10), (k // 2 - 5, k // 2 + 5), (steps - 10, steps)]:
+    dd = [(t[:, lo:hi, i + 1] - t[:, lo:hi, i]).mean() for i in range(6)]
+    print(f"  steps {lo:3d}-{hi:3d}: " + " ".join(f"{x:7.0f}" for x in dd))
