@@ -522,7 +522,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                     if (i == first) al = y;
                     else tl = fma(y, y, tl);
                 }
-                al = __shfl_sync(kFull, al, first & 31);  // row `first` lives in lane first % 32
+                al = __shfl_sync(kFull, al, 0);  // row `first` is lane 0's first row
                 tl = warp_sum(tl);
                 double tu, be, sc;
                 reflector(al, tl, m - first, tu, be, sc);
