@@ -168,6 +168,21 @@ IDK_API int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch,
 IDK_API int idk_id_from_sketch(idk_handle h, double* d_y, int64_t l, int64_t n, int64_t ldy, int64_t k,
                                int64_t c_begin, int64_t c_end, int64_t* d_cols, double* d_z_local);
 
+/* Concurrent entry for a stream of independent IDs (serving): `count` m x n
+ * matrices d_a[i] (device, lda), results into d_cols[i], d_z[i] (k * max(m, n))
+ * and, if d_c != NULL, d_c[i].  ID i runs on lane i % L (L = min(count,
+ * idk_set_concurrency), default 8), each lane a non-blocking stream with its own
+ * workspace, so one ID's CPQR (a 16-SM cluster at cfg2) overlaps other IDs'
+ * sketch GEMMs and CPQRs.  Lanes start after the work already queued on the
+ * handle's stream; the call returns after all IDs finished.  seeds[i] (host
+ * array) or 0 when seeds == NULL.  Statuses are checked at the end; the first
+ * failure is reported with its index. */
+IDK_API int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int64_t m, int64_t n,
+                              int64_t lda, int64_t k, int method, const uint64_t* seeds, int64_t p, int omega_mode,
+                              int64_t* const* d_cols, double* const* d_z, double* const* d_c, int* transposed);
+/* Number of concurrent lanes of idk_id_auto_batch (1..64, default 8). */
+IDK_API int idk_set_concurrency(idk_handle h, int lanes);
+
 /* ---- stages / primitives (device pointers) ---------------------------------- */
 
 /* Omega (l x m, ld = l) = Philox Gaussian, keyed by seed (mirrors idko_omega_philox). */

@@ -30,6 +30,9 @@ SIGNATURES = {
     "idk_stage_times": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int]),
     "idk_optim_id": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "idk_sketch_rid": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _I64, _I64, C.c_uint64, C.c_int, _P, _P, _P, _P]),
+    "idk_id_auto_batch": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, C.c_int, _P, _I64, C.c_int, _P, _P, _P,
+                                    C.POINTER(C.c_int)]),
+    "idk_set_concurrency": (C.c_int, [_P, C.c_int]),
     "idk_optim_rid": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _I64, C.c_double, C.c_uint64, _P, _P, _P]),
     "idk_id_auto": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P, _P,
                               C.POINTER(C.c_int)]),

@@ -45,6 +45,11 @@ struct idk_context {
     cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out[2] = {};
     int* h_status_many = nullptr;
     int64_t h_status_many_cap = 0;
+    // concurrent batch entry: child contexts, one stream + workspace each
+    int lanes = 8;
+    std::vector<idk_context*> kids;
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_join;
     // per-stage CUDA events on the launching stream (idk_set_profiling)
     bool profiling = false;
     cudaEvent_t ev[6] = {};
@@ -486,6 +491,13 @@ int idk_create(idk_handle* out, int device) {
 int idk_destroy(idk_handle h) {
     if (!h) return IDK_OK;
     cudaStreamSynchronize(h->stream);
+    for (idk_context* kid : h->kids) {
+        cudaStream_t ks = kid->stream;
+        idk_destroy(kid);
+        cudaStreamDestroy(ks);
+    }
+    for (cudaEvent_t e : h->ev_join) cudaEventDestroy(e);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ws) cudaFree(h->ws);
     if (h->io) cudaFree(h->io);
     if (h->h_status) cudaFreeHost(h->h_status);
@@ -875,6 +887,104 @@ int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a,
             return set_err(h, det ? IDK_ERR_NOT_POSDEF : IDK_ERR_SINGULAR,
                            "id_auto_host_many: matrix " + std::to_string(i) + ": R11 diagonal " +
                                std::to_string(bad) + " is zero");
+        }
+    }
+    return IDK_OK;
+}
+
+int idk_set_concurrency(idk_handle h, int lanes) {
+    if (!h || lanes < 1 || lanes > 64) return IDK_ERR_INVALID_ARG;
+    h->lanes = lanes;
+    return IDK_OK;
+}
+
+int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int64_t m, int64_t n, int64_t lda,
+                      int64_t k, int method, const uint64_t* seeds, int64_t p, int omega_mode,
+                      int64_t* const* d_cols, double* const* d_z, double* const* d_c, int* transposed) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (count < 0 || (count > 0 && (!d_a || !d_cols || !d_z)))
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_auto_batch: bad arguments");
+    int rc = check_k(h, m, n, k, "id_auto");
+    if (rc) return rc;
+    if (omega_mode == IDK_OMEGA_VERBATIM)
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_auto_batch: verbatim omega needs idk_id_auto");
+    if (count == 0) return IDK_OK;
+    // child contexts: one non-blocking stream and one workspace per lane
+    const int L = static_cast<int>(std::min<int64_t>(h->lanes, count));
+    while (static_cast<int>(h->kids.size()) < L) {
+        idk_context* kid = nullptr;
+        if ((rc = idk_create(&kid, h->device))) return set_err(h, rc, "id_auto_batch: lane context creation failed");
+        cudaStream_t ks;
+        if (cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking) != cudaSuccess) {
+            idk_destroy(kid);
+            return set_err(h, IDK_ERR_CUDA, "id_auto_batch: stream creation failed");
+        }
+        kid->stream = ks;
+        h->kids.push_back(kid);
+        cudaEvent_t e;
+        IDK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_join.push_back(e);
+    }
+    if (!h->ev_fork) IDK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    if (count > h->h_status_many_cap) {
+        if (h->h_status_many) cudaFreeHost(h->h_status_many);
+        h->h_status_many = nullptr;
+        h->h_status_many_cap = 0;
+        IDK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->h_status_many), sizeof(int) * count));
+        h->h_status_many_cap = count;
+    }
+    // inputs written on the caller's stream are visible to every lane
+    IDK_CUDA(cudaEventRecord(h->ev_fork, h->stream));
+    std::vector<int64_t> before(static_cast<size_t>(L));
+    for (int l = 0; l < L; ++l) {
+        idk_context* kid = h->kids[static_cast<size_t>(l)];
+        kid->cpqr_mode = h->cpqr_mode;
+        kid->batched_exact = h->batched_exact;
+        if (h->profiling && !kid->ev[0])
+            for (auto& e : kid->ev) IDK_CUDA(cudaEventCreate(&e));
+        kid->profiling = h->profiling;
+        before[static_cast<size_t>(l)] = kid->launches;
+        IDK_CUDA(cudaStreamWaitEvent(kid->stream, h->ev_fork, 0));
+    }
+    int first_rc = IDK_OK;
+    int64_t issued = 0;
+    for (int64_t i = 0; i < count && first_rc == IDK_OK; ++i, ++issued) {
+        idk_context* kid = h->kids[static_cast<size_t>(i % L)];
+        h->h_status_many[i] = 0x7f7f7f7f;
+        kid->async_status = h->h_status_many + i;
+        int tr = 0;
+        rc = id_auto_dev(kid, d_a[i], m, n, lda, k, method, seeds ? seeds[i] : 0, p, omega_mode, nullptr, d_cols[i],
+                         d_z[i], d_c ? d_c[i] : nullptr, &tr);
+        kid->async_status = nullptr;
+        if (transposed) *transposed = tr;
+        if (rc) {
+            first_rc = set_err(h, rc, "id_auto_batch: matrix " + std::to_string(i) + ": " + kid->err);
+        }
+    }
+    for (int l = 0; l < L; ++l) {
+        idk_context* kid = h->kids[static_cast<size_t>(l)];
+        IDK_CUDA(cudaEventRecord(h->ev_join[static_cast<size_t>(l)], kid->stream));
+        IDK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join[static_cast<size_t>(l)], 0));
+        h->launches += kid->launches - before[static_cast<size_t>(l)];
+    }
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->profiling) {  // stage times of each lane's last ID, averaged over the lanes
+        for (float& v : h->stage_ms) v = 0.f;
+        for (int l = 0; l < L; ++l) {
+            idk_context* kid = h->kids[static_cast<size_t>(l)];
+            collect_stage_times(kid);
+            for (int j = 0; j < 5; ++j) h->stage_ms[j] += kid->stage_ms[j] / static_cast<float>(L);
+        }
+    }
+    if (first_rc) return first_rc;
+    for (int64_t i = 0; i < issued; ++i) {
+        const int bad = h->h_status_many[i];
+        if (bad != 0x7f7f7f7f) {
+            const bool det = method == 0;
+            return set_err(h, det ? IDK_ERR_NOT_POSDEF : IDK_ERR_SINGULAR,
+                           "id_auto_batch: matrix " + std::to_string(i) + ": zero pivot at index " +
+                               std::to_string(bad));
         }
     }
     return IDK_OK;

@@ -323,6 +323,43 @@ def id_auto_many(mats, k: int, method: int = DETERMINISTIC, seed: int = 0, p: in
     return cols, zs, cs, bool(tr.value)
 
 
+def id_auto_batch(mats, k: int, method: int = DETERMINISTIC, seeds=None, p: int = 0,
+                  omega_mode: int = OMEGA_PHILOX, want_c: bool = True, out=None, lanes: int = None):
+    """Concurrent device entry (idk_id_auto_batch): IDs of several same-shape
+    fp64 CUDA matrices, spread over `lanes` streams so one ID's CPQR overlaps
+    the others' GEMMs.  `seeds`: one per matrix (default 0).  `p`: sketch
+    oversampling (RANDOMIZED) or extra sampled columns floor(fraction*k)
+    (SAMPLED), as in the C ABI.  `out` (optional) =
+    preallocated (cols, z, c) lists.  Returns (cols, z, c, transposed)."""
+    import torch
+    mats = [fortran(x) for x in mats]
+    cnt = len(mats)
+    m, n = mats[0].shape
+    if any(tuple(x.shape) != (m, n) or _ld(x) != _ld(mats[0]) for x in mats):
+        raise InvalidArgument("id_auto_batch: all matrices must have the same shape and leading dimension")
+    tall = m > n
+    zc, crow = (m, n) if tall else (n, m)
+    dev = mats[0].device
+    if out is None:
+        cols = [torch.empty(k, dtype=torch.int64, device=dev) for _ in range(cnt)]
+        zs = [empty_f(k, zc, dev) for _ in range(cnt)]
+        cs = [empty_f(crow, k, dev) for _ in range(cnt)] if want_c else None
+    else:
+        cols, zs, cs = out
+    P = C.c_void_p * max(cnt, 1)
+    ctx = context(dev.index or 0)
+    ctx.bind_stream()
+    if lanes is not None:
+        ctx.check(ctx.lib.idk_set_concurrency(ctx.h, lanes))
+    sd = (C.c_uint64 * max(cnt, 1))(*(list(seeds) if seeds is not None else [0] * cnt))
+    tr = C.c_int(0)
+    ctx.check(ctx.lib.idk_id_auto_batch(ctx.h, cnt, P(*[x.data_ptr() for x in mats]), m, n, _ld(mats[0]), k, method,
+                                        sd, p, omega_mode, P(*[x.data_ptr() for x in cols]),
+                                        P(*[x.data_ptr() for x in zs]),
+                                        P(*[x.data_ptr() for x in cs]) if cs is not None else None, C.byref(tr)))
+    return cols, zs, cs, bool(tr.value)
+
+
 def optim_id_batched(a, k: int, want_c: bool = True):
     """BASELINE cfg3: `a` is a (batch, n, m) contiguous CUDA tensor holding
     batch column-major m x n matrices (i.e. a[b].t() is matrix b).

@@ -328,6 +328,31 @@ def test_pipelined_host_entry_reports_failing_index(idk, oracle):
         idk.id_auto_many([good, good, bad, good], 3, idk.DETERMINISTIC)
 
 
+@pytest.mark.parametrize("method", [0, 1, 2])
+@pytest.mark.parametrize("shape,k", [((110, 4000), 100), ((60, 90), 8), ((90, 60), 8)])
+def test_concurrent_batch_entry_matches_single_calls(idk, oracle, method, shape, k):
+    """idk_id_auto_batch: 11 IDs over 4 lanes give the bit-identical results of
+    single idk_id_auto calls (same kernels, same per-ID workspace layout)."""
+    mats = [dev(oracle.gaussian_matrix(shape[0], shape[1], 40 + s)) for s in range(11)]
+    seeds = [100 + s for s in range(11)]
+    cols, zs, cs, tr = idk.id_auto_batch(mats, k, method, seeds=seeds, p=5, lanes=4)
+    assert tr == (shape[0] > shape[1])
+    for x, sd, c_, z_, cc in zip(mats, seeds, cols, zs, cs):
+        r = idk.id_auto(x, k, method, seed=sd, p=5, oversampling_fraction=5 / k if method == 2 else None)
+        assert np.array_equal(host(c_), host(r.cols))
+        assert np.array_equal(host(z_), host(r.z))
+        assert np.array_equal(host(cc), host(r.c))
+
+
+def test_concurrent_batch_entry_reports_failing_index(idk, oracle):
+    good = dev(oracle.gaussian_matrix(10, 12, 1))
+    bad = np.zeros((10, 12))
+    g = oracle.gaussian_matrix(10, 2, 8)
+    bad[:, 3], bad[:, 9] = g[:, 0], g[:, 1]
+    with pytest.raises(idk.NotPositiveDefiniteError, match="matrix 2"):
+        idk.id_auto_batch([good, good, dev(bad), good], 3, idk.DETERMINISTIC, lanes=3)
+
+
 @pytest.mark.parametrize("shape,k,method", [((40, 70), 9, 0), ((300, 500), 40, 1), ((900, 120), 16, 1), ((120, 90), 7, 0)])
 def test_diagnostics_and_approx_match_reference(idk, ref, shape, k, method):
     """id.cpp:97-122 on the device (fused residual) vs the reference's diagnostics."""
