@@ -329,6 +329,7 @@ def run_ours(args):
         e2e_val = ids / (float(e_ms.item()) / 1e3)
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "h2d_gbs": e2e_val / max(ids / ke, 1) * h2d / 1e9,
+               "h2d_peak_gbs": 55.1, "h2d_peak_source": "profiles/probe_h2d_r01.txt (pinned H2D, measured)",
                "api": ("paper_2105_07076_b200.sharded.sketch_rid_sharded (per-rank shard, pinned host)" if use_sharded
                        else "idk_id_auto_host_many (include/idkit_b200.h): pinned host buffers, upload/compute/"
                             "download overlapped across steps")}
