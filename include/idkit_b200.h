@@ -198,6 +198,11 @@ IDK_API int idk_sketch(idk_handle h, const double* d_omega, int64_t l, const dou
 IDK_API int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, int64_t steps,
                           double* d_q, double* d_r, int64_t* d_perm);
 
+/* Host-buffer form of idk_qr_column_pivoted (qr.hpp:34): h_a m x n (ld = m);
+ * h_q m x steps, h_r steps x n, h_perm n (each may be NULL). */
+IDK_API int idk_qr_column_pivoted_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t steps,
+                                       double* h_q, double* h_r, int64_t* h_perm);
+
 /* idkit::select_columns (matrix.hpp:76, matrix.cpp:121-130): out (m x ncols)
  * = A[:, cols]; rows_of_a != 0 gathers rows instead (out is n x ncols). */
 IDK_API int idk_select_columns(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, const int64_t* d_cols,
@@ -223,6 +228,24 @@ IDK_API int idk_diagnostics(idk_handle h, const double* d_a, int64_t m, int64_t 
  * part of the call.  h_a is m x n (ld = m); h_z holds k * max(m, n). */
 IDK_API int idk_id_auto_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int method, uint64_t seed,
                      int64_t p, int omega_mode, int64_t* h_cols, double* h_z, double* h_c, int* transposed);
+
+/* optim_id / optim_rid with host buffers (the reference's value semantics,
+ * id.hpp:40 and :47-48): h_a is m x n (ld = m); h_z is k x n; h_c (optional)
+ * m x k; h_approx (optional) m x n = IdResult::approx (id.cpp:42,73) computed
+ * on the device by idk_matmul_ref, i.e. bit-identical to the reference's
+ * matmul(select_columns(a, cols), z).  No orientation dispatch -- that is
+ * idk_id_auto_host. */
+IDK_API int idk_optim_id_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int64_t* h_cols,
+                              double* h_z, double* h_c, double* h_approx);
+IDK_API int idk_optim_rid_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k,
+                               double oversampling_fraction, uint64_t seed, int64_t* h_cols, double* h_z,
+                               double* h_c, double* h_approx);
+/* idkit::matmul (matrix.hpp:56, matrix.cpp:28-48) in the reference's exact
+ * arithmetic (same summation order, zero skipping, unfused IEEE ops):
+ * C (m x n, ldc) = A (m x k, lda) * B (k x n, ldb), bit-identical to the CPU
+ * reference.  Device pointers. */
+IDK_API int idk_matmul_ref(idk_handle h, const double* d_a, int64_t m, int64_t k, int64_t lda, const double* d_b,
+                           int64_t n, int64_t ldb, double* d_c, int64_t ldc);
 
 /* Pipelined host entry: `count` independent IDs of m x n matrices h_a[i]
  * (host, ld = m), results into h_cols[i], h_z[i] (k * max(m, n)) and, if

@@ -1,0 +1,157 @@
+// idkit_b200_shim.cpp -- the reference-side binding of the drop-in.
+//
+// Compiled against the reference's own headers (proj/include/idkit/*.hpp) in
+// place of its src/id.cpp and src/qr.cpp, it keeps every public signature of
+// the hot path --
+//   optim_id            id.hpp:40      (id.cpp:29-45)
+//   optim_rid           id.hpp:47-48   (id.cpp:47-76)
+//   id_auto             id.hpp:55-56   (id.cpp:78-95)
+//   diagnostics         id.hpp:60      (id.cpp:97-122)
+//   qr_column_pivoted   qr.hpp:34      (qr.cpp:42-126)
+// -- and forwards the work to the C ABI of libidkit_b200.so
+// (include/idkit_b200.h).  Everything else (Matrix, matmul, the solvers, svd,
+// datasets, bench's run_cell, acceptance) is the reference's code, unchanged,
+// so its callers relink without edits (oracle/Makefile target `dropin`).
+//
+// Value semantics are the reference's: results are fresh host matrices,
+// errors are the reference's exception types, and `approx` is formed on the
+// device by idk_matmul_ref in matmul's exact arithmetic (matrix.cpp:28-48:
+// same order, zero skipping, unfused), so test_id.cpp:57-68's bit equality
+// frobenius_distance(r.approx, matmul(select_columns(a, r.cols), r.z)) == 0
+// holds against the reference's own CPU matmul.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "idkit/errors.hpp"
+#include "idkit/id.hpp"
+#include "idkit/matrix.hpp"
+#include "idkit/qr.hpp"
+#include "idkit_b200.h"
+
+namespace idkit {
+
+namespace {
+
+idk_handle handle() {
+    thread_local idk_handle h = nullptr;  // handles are per thread (the reference is reentrant)
+    if (!h) {
+        const char* dev = std::getenv("IDK_DEVICE");
+        if (idk_create(&h, dev ? std::atoi(dev) : 0) != IDK_OK)
+            throw std::runtime_error("idkit_b200: no sm_100 GPU available");
+    }
+    return h;
+}
+
+void check(int rc) {
+    if (rc == IDK_OK) return;
+    const std::string msg = idk_last_error(handle());
+    switch (rc) {
+        case IDK_ERR_INVALID_ARG: throw std::invalid_argument(msg);
+        case IDK_ERR_SINGULAR: throw SingularMatrixError(msg);
+        case IDK_ERR_NOT_POSDEF: throw NotPositiveDefiniteError(msg);
+        default: throw std::runtime_error("idkit_b200: " + msg);
+    }
+}
+
+// Shape contract of every ID entry (id.cpp:14-18); the C ABI checks the same
+// and reports the same text, this copy only guards the host-side transpose.
+void rank_contract(const Matrix& a, std::size_t k, const char* op) {
+    const std::size_t lim = std::min(a.rows(), a.cols());
+    if (lim == 0) throw std::invalid_argument(std::string(op) + ": empty matrix");
+    if (k == 0 || k > lim) throw std::invalid_argument(std::string(op) + ": k must lie in [1, min(rows, cols)]");
+}
+
+IdResult finish(const std::vector<int64_t>& cols64, Matrix z, Matrix approx) {
+    IdResult r;
+    r.cols.assign(cols64.begin(), cols64.end());
+    r.z = std::move(z);
+    r.approx = std::move(approx);  // device product in matmul's exact arithmetic (idk_matmul_ref)
+    r.transposed = false;
+    return r;
+}
+
+}  // namespace
+
+IdResult optim_id(const Matrix& a, std::size_t k) {
+    rank_contract(a, k, "optim_id");
+    std::vector<int64_t> cols(k);
+    Matrix z(k, a.cols()), approx(a.rows(), a.cols());
+    check(idk_optim_id_host(handle(), a.data(), static_cast<int64_t>(a.rows()), static_cast<int64_t>(a.cols()),
+                            static_cast<int64_t>(k), cols.data(), z.data(), nullptr, approx.data()));
+    return finish(cols, std::move(z), std::move(approx));
+}
+
+IdResult optim_rid(const Matrix& a, std::size_t k, double oversampling_fraction, std::uint64_t seed) {
+    rank_contract(a, k, "optim_rid");
+    if (!(oversampling_fraction >= 0.0))
+        throw std::invalid_argument("optim_rid: oversampling_fraction must be non-negative");
+    std::vector<int64_t> cols(k);
+    Matrix z(k, a.cols()), approx(a.rows(), a.cols());
+    check(idk_optim_rid_host(handle(), a.data(), static_cast<int64_t>(a.rows()), static_cast<int64_t>(a.cols()),
+                             static_cast<int64_t>(k), oversampling_fraction, seed, cols.data(), z.data(), nullptr,
+                             approx.data()));
+    return finish(cols, std::move(z), std::move(approx));
+}
+
+IdResult id_auto(const Matrix& a, std::size_t k, IdMethod method, std::uint64_t seed, double oversampling_fraction) {
+    rank_contract(a, k, "id_auto");
+    if (a.rows() <= a.cols()) {
+        return method == IdMethod::deterministic ? optim_id(a, k) : optim_rid(a, k, oversampling_fraction, seed);
+    }
+    const Matrix at = transpose(a);
+    IdResult dual = method == IdMethod::deterministic ? optim_id(at, k) : optim_rid(at, k, oversampling_fraction, seed);
+    IdResult out;
+    out.cols = std::move(dual.cols);  // row indices of a
+    out.z = std::move(dual.z);
+    out.approx = transpose(dual.approx);
+    out.transposed = true;
+    return out;
+}
+
+// id.cpp:97-122 semantics on the host result (approx lives on the host): the
+// relative error is measured against result.approx, as the reference does.
+IdDiagnostics diagnostics(const Matrix& a, const IdResult& result) {
+    const bool same_shape = result.approx.rows() == a.rows() && result.approx.cols() == a.cols();
+    if (!same_shape) throw std::invalid_argument("diagnostics: approximation shape disagrees with matrix");
+    if (result.z.rows() != result.cols.size())
+        throw std::invalid_argument("diagnostics: coefficient row count disagrees with cols");
+    IdDiagnostics out;
+    const double na = frobenius_norm(a), gap = frobenius_distance(a, result.approx);
+    if (na > 0.0) out.relative_error = gap / na;
+    else out.relative_error = gap > 0.0 ? std::numeric_limits<double>::infinity() : 0.0;
+    out.max_abs_z = max_abs(result.z);
+    // largest |Z[:, cols] - I| entry
+    double worst = 0.0;
+    std::size_t j = 0;
+    for (const std::size_t c : result.cols) {
+        if (c >= result.z.cols()) throw std::invalid_argument("diagnostics: column index outside coefficient matrix");
+        const double* zc = result.z.col_data(c);
+        for (std::size_t i = 0; i < result.cols.size(); ++i) worst = std::max(worst, std::fabs(zc[i] - (i == j)));
+        ++j;
+    }
+    out.identity_deviation = worst;
+    out.entry_bound_satisfied = out.max_abs_z <= 2.0 + 1e-12;  // id.hpp:26-31
+    return out;
+}
+
+PivotedQr qr_column_pivoted(const Matrix& a, std::size_t max_steps) {
+    if (a.rows() == 0 || a.cols() == 0 || max_steps < 1 || max_steps > std::min(a.rows(), a.cols()))
+        throw std::invalid_argument("qr_column_pivoted: max_steps must lie in [1, min(rows, cols)]");
+    PivotedQr f;
+    f.steps = max_steps;
+    f.q = Matrix(a.rows(), max_steps);
+    f.r = Matrix(max_steps, a.cols());
+    std::vector<int64_t> perm(a.cols());
+    check(idk_qr_column_pivoted_host(handle(), a.data(), static_cast<int64_t>(a.rows()),
+                                     static_cast<int64_t>(a.cols()), static_cast<int64_t>(max_steps), f.q.data(),
+                                     f.r.data(), perm.data()));
+    f.perm.assign(perm.begin(), perm.end());
+    return f;
+}
+
+}  // namespace idkit

@@ -43,11 +43,14 @@ class NotPositiveDefiniteError(OracleError):
 _CODES = {1: InvalidArgument, 2: SingularMatrixError, 3: NotPositiveDefiniteError}
 
 
-def build(ref: bool = True) -> None:
-    """Compile liboracle.so (and oracle/_ref when the reference is present)."""
+def build(ref: bool = True, dropin: bool = False) -> None:
+    """Compile liboracle.so (and oracle/_ref when the reference is present;
+    `dropin` adds the reference's acceptance suite on both libraries)."""
     targets = ["all"]
     if ref and os.path.isdir(REF_SRC):
         targets.append("ref")
+        if dropin:
+            targets.append("dropin")
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

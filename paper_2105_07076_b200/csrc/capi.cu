@@ -703,6 +703,33 @@ int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n,
     return IDK_OK;
 }
 
+int idk_qr_column_pivoted_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t steps, double* h_q,
+                               double* h_r, int64_t* h_perm) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (!h_a) return set_err(h, IDK_ERR_INVALID_ARG, "qr_column_pivoted: null pointer");
+    if (m <= 0 || n <= 0 || steps < 1 || steps > std::min(m, n))
+        return set_err(h, IDK_ERR_INVALID_ARG, "qr_column_pivoted: max_steps must lie in [1, min(rows, cols)]");
+    Carve cv;
+    const size_t aofs = cv.take(sizeof(double) * m * n);
+    const size_t qofs = cv.take(sizeof(double) * m * steps);
+    const size_t rofs = cv.take(sizeof(double) * steps * n);
+    const size_t pofs = cv.take(sizeof(int64_t) * n);
+    int rc = ensure(h, &h->io, &h->io_cap, cv.total);
+    if (rc) return rc;
+    double* d_a = reinterpret_cast<double*>(h->io + aofs);
+    double* d_q = h_q ? reinterpret_cast<double*>(h->io + qofs) : nullptr;
+    double* d_r = h_r ? reinterpret_cast<double*>(h->io + rofs) : nullptr;
+    int64_t* d_perm = reinterpret_cast<int64_t*>(h->io + pofs);
+    IDK_CUDA(cudaMemcpyAsync(d_a, h_a, sizeof(double) * m * n, cudaMemcpyHostToDevice, h->stream));
+    if ((rc = idk_qr_column_pivoted(h, d_a, m, n, m, steps, d_q, d_r, d_perm))) return rc;
+    if (h_q) IDK_CUDA(cudaMemcpyAsync(h_q, d_q, sizeof(double) * m * steps, cudaMemcpyDeviceToHost, h->stream));
+    if (h_r) IDK_CUDA(cudaMemcpyAsync(h_r, d_r, sizeof(double) * steps * n, cudaMemcpyDeviceToHost, h->stream));
+    if (h_perm) IDK_CUDA(cudaMemcpyAsync(h_perm, d_perm, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    return IDK_OK;
+}
+
 int idk_select_columns(idk_handle h, const double* d_a, int64_t m, int64_t n, int64_t lda, const int64_t* d_cols,
                        int64_t ncols, int rows_of_a, double* d_out) {
     if (!h) return IDK_ERR_INVALID_ARG;
@@ -987,6 +1014,73 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
                                std::to_string(bad));
         }
     }
+    return IDK_OK;
+}
+
+// Host-buffer forms of idk_optim_id / idk_optim_rid (value semantics of
+// id.hpp:40,47-48): A uploaded, the ID computed on the handle's stream, cols /
+// Z / C downloaded.  `rid` selects the column-sampling estimator.
+static int host_optim(idk_handle h, bool rid, const double* h_a, int64_t m, int64_t n, int64_t k, double frac,
+                      uint64_t seed, int64_t* h_cols, double* h_z, double* h_c, double* h_approx) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    int rc = check_k(h, m, n, k, rid ? "optim_rid" : "optim_id");
+    if (rc) return rc;
+    if (!h_a || !h_cols || !h_z) return set_err(h, IDK_ERR_INVALID_ARG, "optim: null pointer");
+    if (rid && !(frac >= 0.0))
+        return set_err(h, IDK_ERR_INVALID_ARG, "optim_rid: oversampling_fraction must be non-negative");
+    Carve cv;
+    const size_t aofs = cv.take(sizeof(double) * m * n);
+    const size_t cofs = cv.take(sizeof(int64_t) * k);
+    const size_t zofs = cv.take(sizeof(double) * k * n);
+    const size_t ccofs = cv.take(sizeof(double) * m * k);
+    const size_t apofs = h_approx ? cv.take(sizeof(double) * m * n) : 0;
+    if ((rc = ensure(h, &h->io, &h->io_cap, cv.total))) return rc;
+    double* d_a = reinterpret_cast<double*>(h->io + aofs);
+    int64_t* d_cols = reinterpret_cast<int64_t*>(h->io + cofs);
+    double* d_z = reinterpret_cast<double*>(h->io + zofs);
+    double* d_c = (h_c || h_approx) ? reinterpret_cast<double*>(h->io + ccofs) : nullptr;
+    IDK_CUDA(cudaMemcpyAsync(d_a, h_a, sizeof(double) * m * n, cudaMemcpyHostToDevice, h->stream));
+    if (rid) {
+        const double extra = frac * static_cast<double>(k);
+        const int64_t e = extra >= 9.0e18 ? INT64_MAX / 2 : static_cast<int64_t>(static_cast<uint64_t>(extra));
+        rc = sampled_rid(h, d_a, m, n, m, false, k, e, seed, d_cols, d_z, d_c);
+    } else {
+        rc = det_id(h, d_a, m, n, m, false, k, d_cols, d_z, d_c);
+    }
+    if (rc) return rc;
+    IDK_CUDA(cudaMemcpyAsync(h_cols, d_cols, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaMemcpyAsync(h_z, d_z, sizeof(double) * k * n, cudaMemcpyDeviceToHost, h->stream));
+    if (h_c) IDK_CUDA(cudaMemcpyAsync(h_c, d_c, sizeof(double) * m * k, cudaMemcpyDeviceToHost, h->stream));
+    if (h_approx) {  // id.cpp:42,73: approx = matmul(C, Z), in the reference's exact arithmetic
+        double* d_ap = reinterpret_cast<double*>(h->io + apofs);
+        IDK_CUDA(idk::matmul_ref_order(d_c, m, d_z, k, m, n, static_cast<int>(k), d_ap, m, h->stream));
+        h->launches += 1;
+        IDK_CUDA(cudaMemcpyAsync(h_approx, d_ap, sizeof(double) * m * n, cudaMemcpyDeviceToHost, h->stream));
+    }
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    return IDK_OK;
+}
+
+int idk_optim_id_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int64_t* h_cols, double* h_z,
+                      double* h_c, double* h_approx) {
+    return host_optim(h, false, h_a, m, n, k, 0.0, 0, h_cols, h_z, h_c, h_approx);
+}
+
+int idk_optim_rid_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, double oversampling_fraction,
+                       uint64_t seed, int64_t* h_cols, double* h_z, double* h_c, double* h_approx) {
+    return host_optim(h, true, h_a, m, n, k, oversampling_fraction, seed, h_cols, h_z, h_c, h_approx);
+}
+
+int idk_matmul_ref(idk_handle h, const double* d_a, int64_t m, int64_t k, int64_t lda, const double* d_b, int64_t n,
+                   int64_t ldb, double* d_c, int64_t ldc) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (m < 0 || n < 0 || k < 0 || k > INT_MAX || !d_a || !d_b || !d_c || lda < m || ldb < k || ldc < m)
+        return set_err(h, IDK_ERR_INVALID_ARG, "matmul: bad arguments");
+    IDK_CUDA(idk::matmul_ref_order(d_a, lda, d_b, ldb, m, n, static_cast<int>(k), d_c, ldc, h->stream));
+    h->launches += 1;
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
     return IDK_OK;
 }
 

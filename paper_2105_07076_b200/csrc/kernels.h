@@ -77,6 +77,8 @@ cudaError_t ldlt_solve(const double* F, const void* scratch, int k, int64_t n, d
 cudaError_t map_cols(const long long* sampled, const long long* piv, int k, long long* cols, cudaStream_t stream);
 
 // util.cu
+cudaError_t matmul_ref_order(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M, int64_t N, int K,
+                             double* C, int64_t ldc, cudaStream_t stream);
 cudaError_t transpose_copy(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb,
                            cudaStream_t stream);
 

@@ -19,17 +19,25 @@ namespace idk {
 
 namespace {
 
-constexpr int kLdltThreads = 1024;
+constexpr int kLdltThreads = 512;
 constexpr int kLC = 4;  // right-hand sides per warp in the solve
 
 struct Blk {
     int start, size, swap;
 };
 
-__device__ __forceinline__ double block_max_idx(double v, int idx, double* sv, int* si, int& out_idx) {
-    // max |value| with the smallest index among equals (first strict max, like
-    // the reference's `if (v > colmax)` scan)
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// One CTA.  S (k x k, column-major, ld k) -> symmetrised, factored (lower
+// triangle: L below the pivot blocks, D on them) into F.  Every access of the
+// reference's algorithm is to the lower triangle, so in shared memory the
+// matrix is stored packed by columns (k(k+1)/2 doubles: k <= 234 fits); larger
+// k works on F in global memory (L2).  blocks/nblk out; *status = index of a
+// singular pivot block (left untouched on success).
+//
+// One __syncthreads per 1x1 step: the warp that updates the next pivot column
+// also reduces its column max (first index among equals, solve.cpp:115-125),
+// every thread takes the pivot decision redundantly, and the scaling of the
+// finished column needs no barrier (no later step reads it).
+__device__ __forceinline__ void warp_argmax_first(double& v, int& idx) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, v, o);
@@ -39,111 +47,80 @@ __device__ __forceinline__ double block_max_idx(double v, int idx, double* sv, i
             idx = oi;
         }
     }
-    __syncthreads();
-    if (lane == 0) {
-        sv[wid] = v;
-        si[wid] = idx;
-    }
-    __syncthreads();
-    v = lane < nw ? sv[lane] : -1.0;
-    idx = lane < nw ? si[lane] : INT_MAX;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-        if (ov > v || (ov == v && oi < idx)) {
-            v = ov;
-            idx = oi;
-        }
-    }
-    out_idx = idx;
-    return v;
 }
 
-// One CTA.  S (k x k, column-major, ld k) -> symmetrised, factored in place
-// (lower triangle: L below the pivot blocks, D on them).  blocks/nblk out;
-// *status = index of a singular pivot block (left untouched on success).
+template <bool in_smem>
 __global__ void __launch_bounds__(kLdltThreads)
 ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk* __restrict__ blocks,
-               int* __restrict__ nblk, int* __restrict__ status, bool in_smem) {
+               int* __restrict__ nblk, int* __restrict__ status) {
     extern __shared__ double sm[];
     __shared__ double sv[32];
-    __shared__ int si[32];
-    __shared__ int s_dec[3];  // kstep, kp, stop
-    const int tid = threadIdx.x, T = blockDim.x;
-    double* a = in_smem ? sm : F;
+    __shared__ double s_cm[2];  // max |a(i, kk)|, i > kk, of the next pivot column (by step parity)
+    __shared__ int s_ci[2];
+    const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = T >> 5;
     if (tid == 0) *nblk = 0;  // a failed factorisation leaves the solve a no-op
-    auto at = [&](int i, int j) -> double& { return a[static_cast<int64_t>(j) * k + i]; };
-
-    // symmetrise (solve.cpp:268-270)
-    for (int e = tid; e < k * k; e += T) {
-        const int j = e / k, i = e - j * k;
-        a[e] = 0.5 * (S[e] + S[static_cast<int64_t>(i) * k + j]);
-    }
+    // column j from row 0 (entries i >= j valid): packed in shared memory or F in L2
+    auto colp = [&](int j) -> double* {
+        if constexpr (in_smem) return sm + (j * k - j * (j - 1) / 2 - j);
+        else return F + static_cast<int64_t>(j) * k;
+    };
+    // (i, j) with i >= j
+    auto at = [&](int i, int j) -> double& { return colp(j)[i]; };
+    // symmetrise (solve.cpp:268-270), lower triangle only
+    for (int j = wid; j < k; j += nw)
+        for (int i = j + lane; i < k; i += 32)
+            at(i, j) = 0.5 * (S[static_cast<int64_t>(j) * k + i] + S[static_cast<int64_t>(i) * k + j]);
     __syncthreads();
-    const double alpha = (1.0 + sqrt(17.0)) / 8.0;
-    int kk = 0, nb = 0;
-    while (kk < k) {
-        // column max below the diagonal (solve.cpp:115-125)
+    if (wid == 0) {
         double v = -1.0;
         int idx = INT_MAX;
-        for (int i = kk + 1 + tid; i < k; i += T) {
-            const double x = fabs(at(i, kk));
+        for (int i = 1 + lane; i < k; i += 32) {
+            const double x = fabs(at(i, 0));
             if (x > v) {
                 v = x;
                 idx = i;
             }
         }
-        int imax;
-        double colmax = block_max_idx(v, idx, sv, si, imax);
+        warp_argmax_first(v, idx);
+        if (lane == 0) {
+            s_cm[0] = v;
+            s_ci[0] = idx;
+        }
+    }
+    __syncthreads();
+    const double alpha = (1.0 + sqrt(17.0)) / 8.0;
+    int kk = 0, nb = 0, par = 0;
+    while (kk < k) {
+        double colmax = s_cm[par];
+        int imax = s_ci[par];
         if (colmax < 0.0) {
             colmax = 0.0;
             imax = kk;
         }
-        if (tid == 0) {
-            const double absakk = fabs(at(kk, kk));
-            int kstep = 1, kp = kk, stop = 0;
-            if (fmax(absakk, colmax) == 0.0) {
-                stop = 1;
-            }
-            s_dec[0] = kstep;
-            s_dec[1] = kp;
-            s_dec[2] = stop;
-        }
-        __syncthreads();
-        if (s_dec[2]) {
+        const double absakk = fabs(at(kk, kk));
+        if (fmax(absakk, colmax) == 0.0) {
             if (tid == 0) *status = kk;
             return;
         }
-        const double absakk = fabs(at(kk, kk));
+        int kstep = 1, kp = kk;
         if (absakk < alpha * colmax) {
             // row max of row imax (solve.cpp:133-136)
             double rv = 0.0;
             for (int j = kk + tid; j < imax; j += T) rv = fmax(rv, fabs(at(imax, j)));
             for (int i = imax + 1 + tid; i < k; i += T) rv = fmax(rv, fabs(at(i, imax)));
             rv = warp_max(rv);
+            if (lane == 0) sv[wid] = rv;
             __syncthreads();
-            if ((tid & 31) == 0) sv[tid >> 5] = rv;
-            __syncthreads();
-            if (tid < 32) {
-                double t = tid < T / 32 ? sv[tid] : 0.0;
-                t = warp_max(t);
-                if (tid == 0) {
-                    const double rowmax = t;
-                    int kstep = 1, kp;
-                    if (absakk >= alpha * colmax * (colmax / rowmax)) kp = kk;
-                    else if (fabs(at(imax, imax)) >= alpha * rowmax) kp = imax;
-                    else {
-                        kp = imax;
-                        kstep = 2;
-                    }
-                    s_dec[0] = kstep;
-                    s_dec[1] = kp;
-                }
+            const double rowmax = warp_max(lane < nw ? sv[lane] : 0.0);
+            if (absakk >= alpha * colmax * (colmax / rowmax)) {
+                kp = kk;
+            } else if (fabs(at(imax, imax)) >= alpha * rowmax) {
+                kp = imax;
+            } else {
+                kp = imax;
+                kstep = 2;
             }
-            __syncthreads();
         }
-        const int kstep = s_dec[0], kp = s_dec[1];
         const int kq = kk + kstep - 1;
         if (kp != kq) {  // swap_symmetric_lower(a, kq, kp) (solve.cpp:97-104)
             for (int i = kp + 1 + tid; i < k; i += T) {
@@ -168,6 +145,7 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
             }
             __syncthreads();
         }
+        const int nxt = kk + kstep;  // next pivot column: updated by warp 0, which also reduces its max
         if (kstep == 1) {
             const double d = at(kk, kk);
             if (d == 0.0) {
@@ -175,17 +153,32 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
                 return;
             }
             const double inv = 1.0 / d;
-            // a(i,j) -= a(i,kk) * (a(j,kk) * inv) for kk < j <= i (solve.cpp:158-162)
-            const int r = k - kk - 1;
-            for (int e = tid; e < r * r; e += T) {
-                const int jj = e / r, ii = e - jj * r;
-                if (ii >= jj) {
-                    const int j = kk + 1 + jj, i = kk + 1 + ii;
-                    at(i, j) -= at(i, kk) * (at(j, kk) * inv);
+            // a(i,j) -= a(i,kk) * (a(j,kk) * inv), kk < j <= i (solve.cpp:158-162): a warp per column
+            const double* ck = colp(kk);
+            for (int j = nxt + wid; j < k; j += nw) {
+                const double w = ck[j] * inv;
+                double* cj = colp(j);
+                double v = -1.0;
+                int idx = INT_MAX;
+                for (int i = j + lane; i < k; i += 32) {
+                    const double y = cj[i] - ck[i] * w;
+                    cj[i] = y;
+                    if (j == nxt && i > j && fabs(y) > v) {
+                        v = fabs(y);
+                        idx = i;
+                    }
+                }
+                if (j == nxt) {
+                    warp_argmax_first(v, idx);
+                    if (lane == 0) {
+                        s_cm[par ^ 1] = v;
+                        s_ci[par ^ 1] = idx;
+                    }
                 }
             }
             __syncthreads();
-            for (int i = kk + 1 + tid; i < k; i += T) at(i, kk) *= inv;
+            double* ckw = colp(kk);
+            for (int i = kk + 1 + tid; i < k; i += T) ckw[i] *= inv;  // column kk is final; no reader
         } else {
             const double d21 = at(kk + 1, kk);
             const double d11 = at(kk + 1, kk + 1) / d21;
@@ -196,19 +189,33 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
                 return;
             }
             const double t = 1.0 / det / d21;
-            const int r = k - kk - 2;
-            // w = t * (d11 a(j,k) - a(j,k+1)), w1 = t * (d22 a(j,k+1) - a(j,k)) (solve.cpp:177-184)
-            for (int e = tid; e < r * r; e += T) {
-                const int jj = e / r, ii = e - jj * r;
-                if (ii >= jj) {
-                    const int j = kk + 2 + jj, i = kk + 2 + ii;
-                    const double wk = t * (d11 * at(j, kk) - at(j, kk + 1));
-                    const double wk1 = t * (d22 * at(j, kk + 1) - at(j, kk));
-                    at(i, j) -= at(i, kk) * wk + at(i, kk + 1) * wk1;
+            // w = t (d11 a(j,k) - a(j,k+1)), w1 = t (d22 a(j,k+1) - a(j,k)) (solve.cpp:177-184)
+            const double* ck = colp(kk);
+            const double* ck1 = colp(kk + 1);
+            for (int j = nxt + wid; j < k; j += nw) {
+                const double wk = t * (d11 * ck[j] - ck1[j]);
+                const double wk1 = t * (d22 * ck1[j] - ck[j]);
+                double* cj = colp(j);
+                double v = -1.0;
+                int idx = INT_MAX;
+                for (int i = j + lane; i < k; i += 32) {
+                    const double y = cj[i] - (ck[i] * wk + ck1[i] * wk1);
+                    cj[i] = y;
+                    if (j == nxt && i > j && fabs(y) > v) {
+                        v = fabs(y);
+                        idx = i;
+                    }
+                }
+                if (j == nxt) {
+                    warp_argmax_first(v, idx);
+                    if (lane == 0) {
+                        s_cm[par ^ 1] = v;
+                        s_ci[par ^ 1] = idx;
+                    }
                 }
             }
             __syncthreads();
-            for (int j = kk + 2 + tid; j < k; j += T) {
+            for (int j = nxt + tid; j < k; j += T) {  // columns kk, kk+1 are final; no reader
                 const double wk = t * (d11 * at(j, kk) - at(j, kk + 1));
                 const double wk1 = t * (d22 * at(j, kk + 1) - at(j, kk));
                 at(j, kk) = wk;
@@ -221,63 +228,99 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
             blocks[nb].swap = kp;
         }
         ++nb;
-        kk += kstep;
-        __syncthreads();
+        kk = nxt;
+        par ^= 1;
     }
+    __syncthreads();
     if (in_smem)
-        for (int e = tid; e < k * k; e += T) F[e] = a[e];
+        for (int j = wid; j < k; j += nw)
+            for (int i = j + lane; i < k; i += 32) F[static_cast<int64_t>(j) * k + i] = at(i, j);
     if (tid == 0) *nblk = nb;
 }
 
 // ldlt_solve (solve.cpp:200-258) for n right-hand sides (k x n, ld k), in
-// place.  Warp w owns columns [c0, c0 + kLC) held in shared memory.
-__global__ void __launch_bounds__(128)
-ldlt_solve_kernel(const double* __restrict__ F, const Blk* __restrict__ blocks, const int* __restrict__ nblk_p,
+// place.  Warp w owns kLC columns held in shared memory and updates them
+// together (one L load feeds kLC FMAs); the CTA first stages L's lower
+// triangle packed in shared memory when it fits (kPacked), else L is read from
+// L2.
+template <bool kPacked>
+__global__ void __launch_bounds__(256)
+ldlt_solve_kernel(const double* __restrict__ F, const Blk* __restrict__ blocks_g, const int* __restrict__ nblk_p,
                   int k, int64_t n, double* __restrict__ B) {
     extern __shared__ double sm[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wid) * kLC;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, W = blockDim.x >> 5;
+    const int nb = *nblk_p;
+    double* xs = sm;                                                     // W * kLC * k
+    double* Lp = xs + static_cast<size_t>(W) * kLC * k;                  // k(k+1)/2 when packed
+    Blk* blk = reinterpret_cast<Blk*>(Lp + (kPacked ? static_cast<size_t>(k) * (k + 1) / 2 : 0));
+    auto cstart = [&](int j) { return j * k - j * (j - 1) / 2; };
+    if constexpr (kPacked) {
+        for (int j = wid; j < k; j += W) {
+            const int c0j = cstart(j);
+            for (int i = j + lane; i < k; i += 32) Lp[c0j + i - j] = F[static_cast<int64_t>(j) * k + i];
+        }
+    }
+    for (int b = tid; b < nb; b += blockDim.x) blk[b] = blocks_g[b];
+    __syncthreads();
+    // column j of L from row i on: Lc(j)[i]
+    auto Lc = [&](int j) -> const double* {
+        if constexpr (kPacked) return Lp + cstart(j) - j;
+        else return F + static_cast<int64_t>(j) * k;
+    };
+    const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * W + wid) * kLC;
     if (c0 >= n) return;
     const int nc = static_cast<int>(min(static_cast<int64_t>(kLC), n - c0));
-    double* x = sm + static_cast<size_t>(wid) * kLC * k;  // x[c*k + i]
-    for (int c = 0; c < nc; ++c)
-        for (int i = lane; i < k; i += 32) x[c * k + i] = B[(c0 + c) * k + i];
+    double* x = xs + static_cast<size_t>(wid) * kLC * k;  // x[c*k + i]
+    for (int c = 0; c < kLC; ++c)
+        for (int i = lane; i < k; i += 32) x[c * k + i] = c < nc ? B[(c0 + c) * k + i] : 0.0;
     __syncwarp();
-    const int nb = *nblk_p;
-    auto L = [&](int i, int j) { return F[static_cast<int64_t>(j) * k + i]; };
     // forward: interchange, then eliminate below the block
     for (int b = 0; b < nb; ++b) {
-        const Blk blk = blocks[b];
-        const int kk = blk.start, r = kk + blk.size - 1;
-        if (blk.swap != r && lane < nc) {
+        const Blk bl = blk[b];
+        const int kk = bl.start, r = kk + bl.size - 1;
+        if (bl.swap != r && lane < kLC) {
             const double t = x[lane * k + r];
-            x[lane * k + r] = x[lane * k + blk.swap];
-            x[lane * k + blk.swap] = t;
+            x[lane * k + r] = x[lane * k + bl.swap];
+            x[lane * k + bl.swap] = t;
         }
         __syncwarp();
-        for (int c = 0; c < nc; ++c) {
-            const double bk = x[c * k + kk];
-            const double bk1 = blk.size == 2 ? x[c * k + kk + 1] : 0.0;
-            for (int i = kk + blk.size + lane; i < k; i += 32) {
-                double v = x[c * k + i] - L(i, kk) * bk;
-                if (blk.size == 2) v -= L(i, kk + 1) * bk1;
-                x[c * k + i] = v;
+        double b0[kLC], b1[kLC];
+#pragma unroll
+        for (int c = 0; c < kLC; ++c) {
+            b0[c] = x[c * k + kk];
+            b1[c] = bl.size == 2 ? x[c * k + kk + 1] : 0.0;
+        }
+        const double* l0 = Lc(kk);
+        if (bl.size == 1) {
+            for (int i = kk + 1 + lane; i < k; i += 32) {
+                const double l = l0[i];
+#pragma unroll
+                for (int c = 0; c < kLC; ++c) x[c * k + i] -= l * b0[c];
+            }
+        } else {
+            const double* l1 = Lc(kk + 1);
+            for (int i = kk + 2 + lane; i < k; i += 32) {
+                const double la = l0[i], lb = l1[i];
+#pragma unroll
+                for (int c = 0; c < kLC; ++c) x[c * k + i] -= la * b0[c] + lb * b1[c];
             }
         }
         __syncwarp();
     }
     // block diagonal
-    for (int b = 0; b < nb; ++b) {
-        const Blk blk = blocks[b];
-        const int kk = blk.start;
-        if (lane < nc) {
-            double* xc = x + lane * k;
-            if (blk.size == 1) {
-                xc[kk] /= L(kk, kk);
+    if (lane < kLC) {
+        double* xc = x + lane * k;
+        for (int b = 0; b < nb; ++b) {
+            const Blk bl = blk[b];
+            const int kk = bl.start;
+            const double* l0 = Lc(kk);
+            if (bl.size == 1) {
+                xc[kk] /= l0[kk];
             } else {
-                const double akm1k = L(kk + 1, kk);
-                const double akm1 = L(kk, kk) / akm1k;
-                const double ak = L(kk + 1, kk + 1) / akm1k;
+                const double* l1 = Lc(kk + 1);
+                const double akm1k = l0[kk + 1];
+                const double akm1 = l0[kk] / akm1k;
+                const double ak = l1[kk + 1] / akm1k;
                 const double denom = akm1 * ak - 1.0;
                 const double bkm1 = xc[kk] / akm1k;
                 const double bk = xc[kk + 1] / akm1k;
@@ -289,22 +332,30 @@ ldlt_solve_kernel(const double* __restrict__ F, const Blk* __restrict__ blocks, 
     __syncwarp();
     // backward: x_c -= sum_{i >= below} L(i, c) x_i, then undo the interchange
     for (int b = nb - 1; b >= 0; --b) {
-        const Blk blk = blocks[b];
-        const int kk = blk.start, below = kk + blk.size;
-        for (int c = 0; c < nc; ++c) {
-            for (int cc = kk; cc < below; ++cc) {
-                double acc = 0.0;
-                for (int i = below + lane; i < k; i += 32) acc += L(i, cc) * x[c * k + i];
-                acc = warp_sum(acc);
-                if (lane == 0) x[c * k + cc] -= acc;
+        const Blk bl = blk[b];
+        const int kk = bl.start, below = kk + bl.size;
+        for (int cc = kk; cc < below; ++cc) {
+            const double* lc = Lc(cc);
+            double acc[kLC];
+#pragma unroll
+            for (int c = 0; c < kLC; ++c) acc[c] = 0.0;
+            for (int i = below + lane; i < k; i += 32) {
+                const double l = lc[i];
+#pragma unroll
+                for (int c = 0; c < kLC; ++c) acc[c] = fma(l, x[c * k + i], acc[c]);
             }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int c = 0; c < kLC; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+            if (lane < kLC) x[lane * k + cc] -= acc[lane == 0 ? 0 : lane == 1 ? 1 : lane == 2 ? 2 : 3];
+            __syncwarp();
         }
-        __syncwarp();
-        const int r = kk + blk.size - 1;
-        if (blk.swap != r && lane < nc) {
+        const int r = kk + bl.size - 1;
+        if (bl.swap != r && lane < kLC) {
             const double t = x[lane * k + r];
-            x[lane * k + r] = x[lane * k + blk.swap];
-            x[lane * k + blk.swap] = t;
+            x[lane * k + r] = x[lane * k + bl.swap];
+            x[lane * k + bl.swap] = t;
         }
         __syncwarp();
     }
@@ -324,26 +375,41 @@ size_t ldlt_scratch_bytes(int k) { return sizeof(Blk) * static_cast<size_t>(k) +
 cudaError_t ldlt_factor(const double* S, int k, double* F, void* scratch, int* status, cudaStream_t stream) {
     Blk* blocks = static_cast<Blk*>(scratch);
     int* nblk = reinterpret_cast<int*>(blocks + k);
-    const size_t smem = sizeof(double) * static_cast<size_t>(k) * k;
-    const bool in_smem = smem <= 200 * 1024;
+    const size_t smem = sizeof(double) * static_cast<size_t>(k) * (k + 1) / 2;
+    const bool in_smem = smem <= 220 * 1024;
     if (in_smem) {
-        cudaError_t e = cudaFuncSetAttribute(ldlt_bk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(ldlt_bk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    ldlt_bk_kernel<<<1, kLdltThreads, in_smem ? smem : 0, stream>>>(S, k, F, blocks, nblk, status, in_smem);
+    if (in_smem) ldlt_bk_kernel<true><<<1, kLdltThreads, smem, stream>>>(S, k, F, blocks, nblk, status);
+    else ldlt_bk_kernel<false><<<1, kLdltThreads, 0, stream>>>(S, k, F, blocks, nblk, status);
     return cudaGetLastError();
 }
 
 cudaError_t ldlt_solve(const double* F, const void* scratch, int k, int64_t n, double* B, cudaStream_t stream) {
     const Blk* blocks = static_cast<const Blk*>(scratch);
     const int* nblk = reinterpret_cast<const int*>(blocks + k);
-    const int64_t warps = (n + kLC - 1) / kLC;
-    const size_t smem = sizeof(double) * 4 * kLC * static_cast<size_t>(k);
-    cudaError_t e = cudaFuncSetAttribute(ldlt_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    const size_t cap = 220 * 1024;
+    const size_t lbytes = sizeof(double) * static_cast<size_t>(k) * (k + 1) / 2;
+    const size_t bbytes = sizeof(Blk) * static_cast<size_t>(k);
+    auto xbytes = [&](int W) { return sizeof(double) * static_cast<size_t>(W) * kLC * k; };
+    int W = 8;
+    bool packed = true;
+    while (W > 1 && xbytes(W) + lbytes + bbytes > cap) W >>= 1;
+    if (xbytes(W) + lbytes + bbytes > cap) {  // L does not fit: read it from L2
+        packed = false;
+        W = 8;
+        while (W > 1 && xbytes(W) + bbytes > cap) W >>= 1;
+    }
+    const size_t smem = xbytes(W) + (packed ? lbytes : 0) + bbytes;
+    const int64_t per_cta = static_cast<int64_t>(W) * kLC;
+    const unsigned grid = static_cast<unsigned>((n + per_cta - 1) / per_cta);
+    void (*fn)(const double*, const Blk*, const int*, int, int64_t, double*) =
+        packed ? ldlt_solve_kernel<true> : ldlt_solve_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    ldlt_solve_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, smem, stream>>>(F, blocks, nblk, k, n, B);
+    fn<<<grid, 32 * W, smem, stream>>>(F, blocks, nblk, k, n, B);
     return cudaGetLastError();
 }
 

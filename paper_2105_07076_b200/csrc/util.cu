@@ -1,4 +1,5 @@
-// util.cu -- layout helpers for the id_auto dual (id.cpp:85: transpose(a)).
+// util.cu -- layout helpers for the id_auto dual (id.cpp:85: transpose(a)) and
+// the reference-order product used for IdResult::approx.
 #include "common.cuh"
 
 namespace idk {
@@ -19,7 +20,39 @@ __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int6
         if (i < rows && j < cols) B[i * ldb + j] = tile[threadIdx.x][ii];
     }
 }
+
+// C (M x N) = A (M x K) * B (K x N) with matrix.cpp:28-48's arithmetic: every
+// output starts at +0.0 and accumulates a(i,l)*b(l,j) for l = 0..K-1 in order,
+// skipping b(l,j) == 0, with unfused IEEE multiply and add (the reference is
+// built without FMA).  Bit-identical to the reference's matmul; one thread per
+// output, rows across lanes (coalesced A, broadcast B).
+__global__ void matmul_ref_order_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                                        int64_t ldb, int64_t M, int64_t N, int K, double* __restrict__ C,
+                                        int64_t ldc) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t j = blockIdx.y;
+    if (j >= N) return;
+    const double* bj = B + j * ldb;
+    double acc = 0.0;
+    if (i < M) {
+        const double* ai = A + i;
+        for (int l = 0; l < K; ++l) {
+            const double b = __ldg(bj + l);
+            if (b == 0.0) continue;
+            acc = __dadd_rn(acc, __dmul_rn(ai[static_cast<int64_t>(l) * lda], b));
+        }
+        C[j * ldc + i] = acc;
+    }
+}
 }  // namespace
+
+cudaError_t matmul_ref_order(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M, int64_t N, int K,
+                             double* C, int64_t ldc, cudaStream_t stream) {
+    if (M <= 0 || N <= 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((M + 127) / 128), static_cast<unsigned>(N));
+    matmul_ref_order_kernel<<<grid, 128, 0, stream>>>(A, lda, B, ldb, M, N, K, C, ldc);
+    return cudaGetLastError();
+}
 
 cudaError_t transpose_copy(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb,
                            cudaStream_t stream) {

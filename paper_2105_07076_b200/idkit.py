@@ -166,7 +166,7 @@ def fortran(t):
         raise InvalidArgument("matrices are fp64 (idkit::Matrix stores double)")
     if t.dim() != 2:
         raise InvalidArgument("expected a 2-D matrix")
-    if t.stride(0) == 1 and t.stride(1) >= max(1, t.shape[0]):
+    if (t.stride(0) == 1 or t.shape[0] <= 1) and (t.shape[1] <= 1 or t.stride(1) >= max(1, t.shape[0])):
         return t
     return t.t().contiguous().t()
 
@@ -177,7 +177,8 @@ def empty_f(m: int, n: int, device):
 
 
 def _ld(t) -> int:
-    return max(int(t.stride(1)), 1)
+    # a single column has no meaningful column stride (torch may report 1)
+    return max(int(t.stride(1)), 1) if t.shape[1] > 1 else max(int(t.shape[0]), 1)
 
 
 def _ptr(t):
@@ -358,6 +359,22 @@ def id_auto_batch(mats, k: int, method: int = DETERMINISTIC, seeds=None, p: int 
                                         P(*[x.data_ptr() for x in zs]),
                                         P(*[x.data_ptr() for x in cs]) if cs is not None else None, C.byref(tr)))
     return cols, zs, cs, bool(tr.value)
+
+
+def matmul_ref(a, b):
+    """idkit::matmul (matrix.cpp:28-48) on the device in the reference's exact
+    arithmetic (summation order, zero skipping, no FMA): bit-identical to the
+    CPU reference.  a, b: fp64 CUDA matrices."""
+    a, b = fortran(a), fortran(b)
+    m, k = a.shape
+    if b.shape[0] != k:
+        raise InvalidArgument(f"matmul: inner dimensions disagree ({k} vs {b.shape[0]})")
+    n = b.shape[1]
+    c = empty_f(m, n, a.device)
+    ctx = context(a.device.index or 0)
+    ctx.bind_stream()
+    ctx.check(ctx.lib.idk_matmul_ref(ctx.h, _ptr(a), m, k, _ld(a), _ptr(b), n, _ld(b), _ptr(c), max(m, 1)))
+    return c
 
 
 def optim_id_batched(a, k: int, want_c: bool = True):
