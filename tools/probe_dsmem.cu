@@ -142,6 +142,20 @@ __global__ void __cluster_dims__(G, 1, 1) probe(int variant, int rows, int round
                 if (tid < rows) xb[tid] = src[HDR + tid];
                 __syncthreads();
             }
+        } else if (variant == 9) {
+            const unsigned mb = smem_u32(&mbar[p]);
+            const unsigned per = (HDR + rows) * 8;
+            const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+            if (tid == 0) mbar_expect_tx(mb, (G - 1) * per);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (ln == 0 && w < G - 1) {
+                const int g = w < me ? w : w + 1;
+                const unsigned sa = smem_u32(own);
+                bulk_push(mapa_u32(sa, g), sa, per, mapa_u32(mb, g));
+            }
+            mbar_wait(mb, (phase >> p) & 1u);
+            phase ^= 1u << p;
         } else if (variant == 8) {
             const unsigned mb = smem_u32(&mbar[p]);
             const unsigned per = (HDR + rows) * 8;
@@ -190,9 +204,10 @@ int main() {
     const char* names[] = {"cluster.sync only", "bulk push hdr+rows (2/peer) + mbar", "bulk push 1/peer + mbar",
                            "st.cluster hdr + cluster.sync + ld.cluster rows", "st.cluster hdr+rows + cluster.sync",
                            "bulk push hdr + mbar + ld.cluster rows", "warp0 st.cluster hdr + remote arrive",
-                           "warp0 st.cluster hdr + remote arrive + ld.cluster rows", "warp0 bulk push 1/peer + mbar"};
+                           "warp0 st.cluster hdr + remote arrive + ld.cluster rows", "warp0 bulk push 1/peer + mbar",
+                           "15 warps x 1 bulk push + mbar"};
     for (int rows : {112, 272, 512}) {
-        for (int v = 0; v < 9; ++v) {
+        for (int v = 0; v < 10; ++v) {
             const size_t smem = sizeof(double) * 2 * G * (HDR + rows);
             cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
