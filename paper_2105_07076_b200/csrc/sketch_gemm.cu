@@ -10,8 +10,10 @@
 //                   id.cpp:85)
 // CTA tile BM x 64 x 16 (BM = 16*WM, chosen so BM covers l with little
 // padding), 4 warps in 2 x 2, warp tile (8*WM) x 32 of m8n8k4 DMMA tiles,
-// 3-stage cp.async pipeline, optional split-K with a fixed-order reduction so
+// 2-stage cp.async pipeline (46 KB of shared memory: 4 CTAs per SM), optional split-K with a fixed-order reduction so
 // results are bit-reproducible run to run.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace idk {
@@ -20,7 +22,7 @@ namespace {
 
 constexpr int kBN = 64;
 constexpr int kBK = 16;
-constexpr int kStages = 3;
+constexpr int kStages = 2;
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, bool pred) {
@@ -326,12 +328,16 @@ int sketch_gemm_pick_wm(int M) {
     return best;
 }
 
-// Number of K splits so the grid covers the SMs ~4x.
+// Number of K splits: enough tiles for ~4 waves of 4 CTAs per SM (so the last
+// partial wave costs little) while every split keeps >= 256 of K.  Measured
+// on B200 (tools/time_cpqr.py): cfg4 5.82 -> 4.95 ms with 4 splits, cfg2 0.25 ->
+// 0.095 ms, cfg5 1.47 -> 1.44 ms.  IDK_GEMM_SPLITS overrides (tuning only).
 int sketch_gemm_pick_splits(int M, int64_t N, int64_t K, int num_sms) {
+    if (const char* e = getenv("IDK_GEMM_SPLITS")) return atoi(e) > 0 ? atoi(e) : 1;
     const int wm = sketch_gemm_pick_wm(M);
     const int64_t tiles = ((M + 16 * wm - 1) / (16 * wm)) * ((N + kBN - 1) / kBN);
     int splits = 1;
-    while (tiles * splits < 3LL * num_sms && K / (splits * 2) >= 256 && splits < 16) splits *= 2;
+    while (tiles * splits < 16LL * num_sms && K / (splits * 2) >= 256 && splits < 16) splits *= 2;
     return splits;
 }
 
