@@ -760,14 +760,68 @@ cpqr_resident_kernel(ResidentArgs a) {
         xa = xbuf;
     };
 
+    // Grid round: as in cluster mode, the warp holding the CTA's winner builds
+    // the candidate's updated column with all 32 lanes (its deferred update
+    // applied to a raw copy), writes it to the L2 slot and releases the tagged
+    // record; the other warps apply their deferred axpy while the records fly.
     auto grid_round = [&](int first, bool cand, double lv, long long pos, int step) {
         int winpos, winlc;
         const double mx = cta_argmax(cand, lv, pos, winpos, winlc);
         trace(step, 2);
         const int parity = first & 1;
-        publish(parity, static_cast<unsigned>(first + 1), mx, winpos, winlc, first);
-        trace(step, 3);
-        grid_exchange(parity, static_cast<unsigned>(first + 1), first, cand, lv, pos, step);
+        const unsigned tag = static_cast<unsigned>(first + 1);
+        const bool have = winpos != INT_MAX;
+        const bool pubwarp = wid == (have ? (winlc * S) >> 5 : 0);
+        if (pubwarp) {
+            double* dst = slot_ptr(parity, me);
+            double* xscr = xpull;  // scratch (grid mode keeps the current reflector in xbuf)
+            if (have) {
+                const int wl0 = (winlc * S) & 31;
+                const double ww = __shfl_sync(kFull, todo ? wpend : 0.0, wl0);  // 0: already current
+                if (lc == winlc) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int i = l0 + q + S * r;
+                        if (i >= first && i < m) xscr[i] = yr[r];
+                    }
+                }
+                __syncwarp();
+                const double* wrow = rows + static_cast<size_t>(winlc) * lds;
+                double al = 0.0, tl = 0.0;
+                for (int i = first + lane; i < m; i += 32) {
+                    const double y = fma(-ww, xa[i], i < l0 ? wrow[i] : xscr[i]);  // == the group's own axpy
+                    dst[kHdr + i - first] = y;
+                    if (i == first) al = y;
+                    else tl = fma(y, y, tl);
+                }
+                al = __shfl_sync(kFull, al, 0);
+                tl = warp_sum(tl);
+                if (lane == 0) {
+                    double tu, be, sc;
+                    reflector(al, tl, m - first, tu, be, sc);
+                    dst[0] = __longlong_as_double(c0 + winlc);
+                    dst[1] = tu;
+                    dst[2] = be;
+                    dst[3] = sc;
+                }
+            }
+            __threadfence();  // slot data before the tagged record (release)
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
+                const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
+                unsigned long long* rp = a.rec + (static_cast<size_t>(parity) * G + me) * kRecWords;
+                st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
+                st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
+            }
+            trace_by(lane == 0, step, 3);
+            asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
+        } else {
+            asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+        }
+        do_axpy();
+        trace(step, 7);
+        grid_exchange(parity, tag, first, cand, lv, pos, step);
     };
 
     // ---- pivot 0 ----
@@ -889,7 +943,6 @@ cpqr_resident_kernel(ResidentArgs a) {
             }
             if (q == 0) s_live[lc] = lv;
             cand = q == 0;
-            if constexpr (!kCluster) do_axpy();
         }
         trace(s, 1);
         if (s + 1 == a.k) {
