@@ -229,13 +229,11 @@ cpqr_resident_kernel(ResidentArgs a) {
     const bool push = a.push != 0;
     double* chdr = cslots + 3 * cslot;
 
-    __shared__ double red_d[32];
     __shared__ long long red_l[32];
     __shared__ double s_wv[32];     // per-warp argmax records
     __shared__ unsigned s_wp[32];
     __shared__ unsigned s_wl[32];
-    __shared__ double s_sc[3];      // grid: tau, beta, scale of the current pivot
-    __shared__ long long s_sel[3];  // grid: pivot column, its position before the swap, winning CTA (-2: tie pass)
+    __shared__ long long s_sel[3];  // grid tie pass: -, winning position, winning CTA
     __shared__ unsigned long long s_mbar[2];      // cluster: bulk-push barriers, one per slot parity
     __shared__ double s_rv[kCluster ? 1 : 160];  // grid: the G records of this exchange
     __shared__ unsigned s_rp[kCluster ? 1 : 160];
@@ -672,7 +670,11 @@ cpqr_resident_kernel(ResidentArgs a) {
         if (tid < G) __threadfence();  // acquire: slot data after the records
         __syncthreads();
         trace(step, 4);
-        if (wid == 0) {
+        // every warp reduces the G records from shared memory (identical
+        // result everywhere): no second CTA barrier before the column copy
+        int gsel;
+        unsigned wsel;
+        {
             double v[kRecPerLane];
             unsigned p[kRecPerLane];
 #pragma unroll
@@ -698,47 +700,43 @@ cpqr_resident_kernel(ResidentArgs a) {
                 }
             }
             amb = __any_sync(kFull, amb);
-            const unsigned wb = __reduce_min_sync(kFull, best);
-            if (best == wb && best != 0xffffffffu) {  // unique lane: positions are distinct
-                s_sel[0] = amb ? -2 : 0;
-                s_sel[1] = wb;
-                s_sel[2] = lane + 32 * bt;
-            }
-            if (lane == 0) red_d[0] = vmax;
-        }
-        __syncthreads();
-        trace(step, 5);
-        if (s_sel[0] == -2) {
-            // Exact tie pass: lowest position with sqrt(live) >= the global threshold.
-            const double vmax = red_d[0];
-            int winlc;
-            const int winpos = local_pick(cand, lv, pos, vmax, winlc);
-            publish(2, tag, 0.0, winpos, winlc, first);
-            slot = 2;
-            if (wid == 0) {
-                unsigned b2 = 0xffffffffu;
-                int g2 = -1;
-                for (int g = lane; g < G; g += 32) {
-                    double vv;
-                    unsigned pp;
-                    read_rec(2, g, tag, vv, pp);
-                    if (pp < b2) {
-                        b2 = pp;
-                        g2 = g;
+            wsel = __reduce_min_sync(kFull, best);
+            // positions are distinct, so exactly one lane holds the minimum
+            gsel = static_cast<int>(__reduce_min_sync(
+                kFull, (best == wsel && best != 0xffffffffu) ? static_cast<unsigned>(lane + 32 * bt) : 0xffffffffu));
+            if (amb) {
+                // Exact tie pass: lowest position with sqrt(live) >= the global threshold.
+                int winlc;
+                const int winpos = local_pick(cand, lv, pos, vmax, winlc);
+                publish(2, tag, 0.0, winpos, winlc, first);
+                slot = 2;
+                if (wid == 0) {
+                    unsigned b2 = 0xffffffffu;
+                    int g2 = -1;
+                    for (int g = lane; g < G; g += 32) {
+                        double vv;
+                        unsigned pp;
+                        read_rec(2, g, tag, vv, pp);
+                        if (pp < b2) {
+                            b2 = pp;
+                            g2 = g;
+                        }
+                    }
+                    __threadfence();
+                    const unsigned wb = __reduce_min_sync(kFull, b2);
+                    if (b2 == wb && b2 != 0xffffffffu) {
+                        s_sel[1] = wb;
+                        s_sel[2] = g2;
                     }
                 }
-                __threadfence();
-                const unsigned wb = __reduce_min_sync(kFull, b2);
-                if (b2 == wb && b2 != 0xffffffffu) {
-                    s_sel[0] = 0;
-                    s_sel[1] = wb;
-                    s_sel[2] = g2;
-                }
+                __syncthreads();
+                wsel = static_cast<unsigned>(s_sel[1]);
+                gsel = static_cast<int>(s_sel[2]);
             }
-            __syncthreads();
         }
+        trace(step, 5);
         // All threads: header + winner's column (one round trip), scaled into xbuf by absolute row.
-        const double* src = slot_ptr(slot, static_cast<int>(s_sel[2]));
+        const double* src = slot_ptr(slot, gsel);
         const double h0 = __ldcg(src);
         const double tu = __ldcg(src + 1);
         const double be = __ldcg(src + 2);
@@ -751,10 +749,9 @@ cpqr_resident_kernel(ResidentArgs a) {
             }
             xbuf[i] = x;
         }
-        const long long sel1 = s_sel[1];
         __syncthreads();
         piv = __double_as_longlong(h0);
-        ppos = sel1;
+        ppos = wsel;
         tau = tu;
         beta = be;
         xa = xbuf;
