@@ -279,7 +279,7 @@ def run_ours(args):
         zc = max(cfg.m, cfg.n)
         crow = cfg.n if tall else cfg.m
 
-        ke = max(1, min(args.steps, 20))
+        ke = max(1, min(max(args.steps, 20), 40))  # pipeline fill amortised over >= 20 IDs
         if not use_sharded:
             # pinned outputs so the downloads are asynchronous too
             def pinned_f(rows, cols_):
