@@ -7,6 +7,7 @@
 //   det ID     : copy (or transpose) A -> persistent CPQR(A, k) -> same tail
 //   batched    : one fused kernel, one CTA per matrix
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -976,6 +977,7 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
     }
     int first_rc = IDK_OK;
     int64_t issued = 0;
+    const auto t_enqueue0 = std::chrono::steady_clock::now();
     for (int64_t i = 0; i < count && first_rc == IDK_OK; ++i, ++issued) {
         idk_context* kid = h->kids[static_cast<size_t>(i % L)];
         h->h_status_many[i] = 0x7f7f7f7f;
@@ -991,6 +993,9 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
     }
     for (int l = 0; l < L; ++l) {
         idk_context* kid = h->kids[static_cast<size_t>(l)];
+        if (l == 0 && getenv("IDK_DEBUG_HOST_TIME"))
+            fprintf(stderr, "id_auto_batch: host enqueue of %lld IDs took %.1f us\n", static_cast<long long>(issued),
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_enqueue0).count());
         IDK_CUDA(cudaEventRecord(h->ev_join[static_cast<size_t>(l)], kid->stream));
         IDK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join[static_cast<size_t>(l)], 0));
         h->launches += kid->launches - before[static_cast<size_t>(l)];
