@@ -354,11 +354,32 @@ int sampled_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t
     const int64_t p = std::min(k + extra, n);
     const CpqrChoice ch = choose_cpqr(h, m, p, k);
     if ((rc = check_cpqr_fits(h, m, p, ch))) return rc;
+    // Tall samples: pivoted QR of the p x p factor R0 of A_S (shifted
+    // CholeskyQR3, tsqr.cu) instead of the m x p sample itself.
+    const bool tallq = m >= 8 * p && m >= 512 && p <= 1024;  // measured break-even is near m = 4p
+    const CpqrChoice ch2 = tallq ? choose_cpqr(h, p, p, k) : ch;
+    if (tallq && (rc = check_cpqr_fits(h, p, p, ch2))) return rc;
     const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(k), n, m, h->num_sms);
+    const int gsplits = tallq ? idk::sketch_gemm_pick_splits(static_cast<int>(p), p, m, h->num_sms) : 1;
     Carve cv;
     const size_t sofs = cv.take(sizeof(long long) * p);
     const size_t wofs = cv.take(sizeof(double) * m * p);
     const CpqrWs w = carve_cpqr(cv, m, p, k, h->num_sms, ch);
+    CpqrWs w2 = w;
+    size_t wtofs = 0, gmofs = 0, l1ofs = 0, l2ofs = 0, l3ofs = 0, p1ofs = 0, r0ofs = 0, trofs = 0, stofs = 0, gpofs = 0;
+    if (tallq) {
+        w2 = carve_cpqr(cv, p, p, k, h->num_sms, ch2);
+        wtofs = cv.take(sizeof(double) * m * p);
+        gmofs = cv.take(sizeof(double) * p * p);
+        l1ofs = cv.take(sizeof(double) * p * p);
+        l2ofs = cv.take(sizeof(double) * p * p);
+        l3ofs = cv.take(sizeof(double) * p * p);
+        p1ofs = cv.take(sizeof(double) * p * p);
+        r0ofs = cv.take(sizeof(double) * p * p);
+        trofs = cv.take(sizeof(double));
+        stofs = cv.take(sizeof(int) * 4);
+        gpofs = gsplits > 1 ? cv.take(sizeof(double) * p * p * gsplits) : 0;
+    }
     const size_t cofs = d_c ? 0 : cv.take(sizeof(double) * m * k);
     const size_t ctofs = cv.take(sizeof(double) * m * k);
     const size_t rtofs = cv.take(sizeof(double) * k * k);
@@ -370,15 +391,12 @@ int sampled_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t
     char* base = h->ws;
     long long* sampled = reinterpret_cast<long long*>(base + sofs);
     double* W = reinterpret_cast<double*>(base + wofs);
-    long long* piv = reinterpret_cast<long long*>(base + w.pivots);
-    int* status = reinterpret_cast<int*>(base + w.status);
     double* C = d_c ? d_c : reinterpret_cast<double*>(base + cofs);
     double* Ct = reinterpret_cast<double*>(base + ctofs);
-    double* R11 = reinterpret_cast<double*>(base + w.r11);
     double* R11t = reinterpret_cast<double*>(base + rtofs);
     double* gram = reinterpret_cast<double*>(base + gofs);
     double* F = reinterpret_cast<double*>(base + fofs);
-    const int ki = static_cast<int>(k);
+    const int ki = static_cast<int>(k), pi = static_cast<int>(p);
 
     const size_t idx_bytes = sizeof(long long) * p;
     if (idx_bytes > h->h_idx_cap) {
@@ -393,16 +411,68 @@ int sampled_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t
     host_sample_columns(h->h_idx, n, p, seed);
     mark(h, 0);
     IDK_CUDA(cudaMemcpyAsync(sampled, h->h_idx, idx_bytes, cudaMemcpyHostToDevice, h->stream));
-    IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
     IDK_CUDA(idk::gather_columns(d_a, lda, m, sampled, static_cast<int>(p), trans, W, h->stream));
+    h->launches += 1;
     mark(h, 1);
+    // the matrix the pivoted QR runs on: the sample, or its R factor
+    double* Wc = W;
+    int64_t mc = m;
+    CpqrChoice chc = ch;
+    CpqrWs wc = w;
+    if (tallq) {
+        double* Wt = reinterpret_cast<double*>(base + wtofs);
+        double* Gm = reinterpret_cast<double*>(base + gmofs);
+        double* L1 = reinterpret_cast<double*>(base + l1ofs);
+        double* L2 = reinterpret_cast<double*>(base + l2ofs);
+        double* L3 = reinterpret_cast<double*>(base + l3ofs);
+        double* P1 = reinterpret_cast<double*>(base + p1ofs);
+        double* R0 = reinterpret_cast<double*>(base + r0ofs);
+        double* tr = reinterpret_cast<double*>(base + trofs);
+        int* st = reinterpret_cast<int*>(base + stofs);
+        double* gpart = gsplits > 1 ? reinterpret_cast<double*>(base + gpofs) : nullptr;
+        IDK_CUDA(cudaMemsetAsync(st, 0x7f, sizeof(int) * 3, h->stream));
+        IDK_CUDA(cudaMemsetAsync(st + 3, 0, sizeof(int), h->stream));
+        IDK_CUDA(idk::transpose_copy(W, m, m, p, Wt, p, h->stream));
+        // G1 = A_S^T A_S (+ shift 11 (mp + p(p+1)) u ||A_S||_F^2), Cholesky, Q1^T = L1^-1 A_S^T
+        IDK_CUDA(idk::sketch_gemm(Wt, p, W, m, false, Gm, p, pi, p, m, gsplits, gpart, h->stream));
+        IDK_CUDA(idk::gram_trace(Gm, pi, tr, st + 3, h->stream));
+        const double shift_factor = 11.0 * (static_cast<double>(m) * p + static_cast<double>(p) * (p + 1)) * 0x1.0p-53;
+        IDK_CUDA(idk::cholesky_lower(Gm, pi, tr, shift_factor, L1, st, h->stream));
+        IDK_CUDA(idk::trsv_lower_many(L1, pi, m, Wt, h->stream));
+        // two plain Cholesky QR steps on Q1
+        IDK_CUDA(idk::sketch_gemm(Wt, p, Wt, p, true, Gm, p, pi, p, m, gsplits, gpart, h->stream));
+        IDK_CUDA(idk::cholesky_lower(Gm, pi, nullptr, 0.0, L2, st + 1, h->stream));
+        IDK_CUDA(idk::trsv_lower_many(L2, pi, m, Wt, h->stream));
+        IDK_CUDA(idk::sketch_gemm(Wt, p, Wt, p, true, Gm, p, pi, p, m, gsplits, gpart, h->stream));
+        IDK_CUDA(idk::cholesky_lower(Gm, pi, nullptr, 0.0, L3, st + 2, h->stream));
+        // R0 = L3^T L2^T L1^T = (L1 L2 L3)^T
+        IDK_CUDA(idk::sketch_gemm(L1, p, L2, p, false, P1, p, pi, p, p, 1, nullptr, h->stream));
+        IDK_CUDA(idk::sketch_gemm(P1, p, L3, p, false, Gm, p, pi, p, p, 1, nullptr, h->stream));
+        IDK_CUDA(idk::transpose_copy(Gm, p, p, p, R0, p, h->stream));
+        h->launches += 16 + (gsplits > 1 ? 3 : 0);
+        int hst[4];
+        IDK_CUDA(cudaMemcpyAsync(hst, st, sizeof(hst), cudaMemcpyDeviceToHost, h->stream));
+        IDK_CUDA(cudaStreamSynchronize(h->stream));
+        // an exactly zero sampled column (the reference's rank-deficiency case) or a
+        // failed Cholesky: keep the reference's own route, the pivoted QR of A_S
+        if (hst[0] == 0x7f7f7f7f && hst[1] == 0x7f7f7f7f && hst[2] == 0x7f7f7f7f && hst[3] == 0) {
+            Wc = R0;
+            mc = p;
+            chc = ch2;
+            wc = w2;
+        }
+    }
+    long long* piv = reinterpret_cast<long long*>(base + wc.pivots);
+    int* status = reinterpret_cast<int*>(base + wc.status);
+    double* R11 = reinterpret_cast<double*>(base + wc.r11);
+    IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
     mark(h, 2);
-    IDK_CUDA(run_cpqr(h, ch, W, m, p, k, base, w));
+    IDK_CUDA(run_cpqr(h, chc, Wc, mc, p, k, base, wc));
     mark(h, 3);
     IDK_CUDA(idk::map_cols(sampled, piv, ki, reinterpret_cast<long long*>(d_cols), h->stream));
     IDK_CUDA(idk::gather_columns(d_a, lda, m, reinterpret_cast<const long long*>(d_cols), ki, trans, C, h->stream));
     // gram = R_k^T R_k, rhs = C^T M (written straight into Z), both on the DMMA pipe
-    IDK_CUDA(idk::gather_r11(W, m, piv, ki, R11, h->stream));
+    IDK_CUDA(idk::gather_r11(Wc, mc, piv, ki, R11, h->stream));
     IDK_CUDA(idk::transpose_copy(R11, k, k, k, R11t, k, h->stream));
     IDK_CUDA(idk::sketch_gemm(R11t, k, R11, k, false, gram, k, ki, k, k, 1, nullptr, h->stream));
     IDK_CUDA(idk::transpose_copy(C, m, m, k, Ct, k, h->stream));
@@ -412,7 +482,7 @@ int sampled_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t
     IDK_CUDA(idk::ldlt_solve(F, base + lofs, ki, n, d_z, h->stream));
     mark(h, 4);
     mark(h, 5);
-    h->launches += 11 + (splits > 1 ? 1 : 0);
+    h->launches += 10 + (splits > 1 ? 1 : 0);
     if (h->async_status) {
         IDK_CUDA(cudaMemcpyAsync(h->async_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         return IDK_OK;

@@ -76,6 +76,12 @@ cudaError_t ldlt_factor(const double* S, int k, double* F, void* scratch, int* s
 cudaError_t ldlt_solve(const double* F, const void* scratch, int k, int64_t n, double* B, cudaStream_t stream);
 cudaError_t map_cols(const long long* sampled, const long long* piv, int k, long long* cols, cudaStream_t stream);
 
+// tsqr.cu (shifted CholeskyQR3 R factor of a tall sample, for optim_rid)
+cudaError_t cholesky_lower(const double* G, int p, const double* trace, double shift_factor, double* L, int* status,
+                           cudaStream_t stream);
+cudaError_t trsv_lower_many(const double* L, int p, int64_t n, double* X, cudaStream_t stream);
+cudaError_t gram_trace(const double* G, int p, double* out, int* zero_col, cudaStream_t stream);
+
 // util.cu
 cudaError_t matmul_ref_order(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M, int64_t N, int K,
                              double* C, int64_t ldc, cudaStream_t stream);
