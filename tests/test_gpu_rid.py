@@ -135,3 +135,29 @@ def test_id_auto_sampled_vs_reference(idk, ref, m, n):
     # the host-buffer entry gives the same result
     h = idk.id_auto(a, k, idk.SAMPLED, seed=77)
     assert np.array_equal(h.cols, rcols) and rel(h.z, rz) <= ZTOL
+
+
+@pytest.mark.parametrize("m,n,k,frac,decay,seed", [
+    (3000, 400, 30, 0.5, 6.0, 41),    # tall sample: p = 45, pivoted QR on the CholeskyQR3 factor
+    (2500, 120, 40, 1.0, 9.0, 42),    # column norms down to 1e-9: the shifted first step matters
+])
+def test_optim_rid_tall_sample_vs_reference(idk, ref, m, n, k, frac, decay, seed):
+    a = ref.gaussian_matrix(m, n, seed) * np.logspace(0, -decay, n)[None, :]
+    a = np.asfortranarray(a)
+    r = idk.optim_rid(dev(a), k, frac, seed)
+    rcols, rz, rapprox = ref.optim_rid(a, k, frac, seed)
+    assert np.array_equal(host(r.cols), rcols)
+    c = a[:, rcols]
+    s = np.linalg.svd(np.linalg.qr(c, mode="r"), compute_uv=False)
+    kappa2 = (s[0] / s[-1]) ** 2
+    assert rel(host(r.z), rz) <= max(ZTOL, 64 * EPS * kappa2)
+
+
+def test_optim_rid_tall_sample_with_zero_columns(idk, ref):
+    """An exactly zero sampled column keeps the reference's route (pivoted QR of A_S)."""
+    a = np.asfortranarray(ref.gaussian_matrix(2000, 60, 43))
+    a[:, ::3] = 0.0
+    r = idk.optim_rid(dev(a), 8, 1.0, 44)
+    rcols, rz, _ = ref.optim_rid(a, 8, 1.0, 44)
+    assert np.array_equal(host(r.cols), rcols)
+    assert rel(host(r.z), rz) <= ZTOL
