@@ -29,8 +29,8 @@ struct Blk {
 // One CTA.  S (k x k, column-major, ld k) -> symmetrised, factored (lower
 // triangle: L below the pivot blocks, D on them) into F.  Every access of the
 // reference's algorithm is to the lower triangle, so in shared memory the
-// matrix is stored packed by columns (k(k+1)/2 doubles: k <= 234 fits); larger
-// k works on F in global memory (L2).  blocks/nblk out; *status = index of a
+// matrix is stored packed by columns (k(k+1)/2 doubles: k <= 234 fits); for
+// larger k the first steps work on F in L2 until the trailing triangle fits.  blocks/nblk out; *status = index of a
 // singular pivot block (left untouched on success).
 //
 // One __syncthreads per 1x1 step: the warp that updates the next pivot column
@@ -49,20 +49,38 @@ __device__ __forceinline__ void warp_argmax_first(double& v, int& idx) {
     }
 }
 
-template <bool in_smem>
+// Storage: the working lower triangle starts in F (L2); once the trailing
+// triangle from the current step on fits in shared memory (`switch_at`, 0 when
+// the whole matrix fits) it is moved there, packed by columns, and the
+// remaining steps run on chip.  Every step touches only columns >= its own.
 __global__ void __launch_bounds__(kLdltThreads)
 ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk* __restrict__ blocks,
-               int* __restrict__ nblk, int* __restrict__ status) {
+               int* __restrict__ nblk, int* __restrict__ status, int switch_at) {
     extern __shared__ double sm[];
     __shared__ double sv[32];
     __shared__ double s_cm[2];  // max |a(i, kk)|, i > kk, of the next pivot column (by step parity)
     __shared__ int s_ci[2];
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = T >> 5;
     if (tid == 0) *nblk = 0;  // a failed factorisation leaves the solve a no-op
-    // column j from row 0 (entries i >= j valid): packed in shared memory or F in L2
+    int s0 = INT_MAX;  // first column held in shared memory (after the switch)
+    // column j from row 0 (entries i >= j valid)
     auto colp = [&](int j) -> double* {
-        if constexpr (in_smem) return sm + (j * k - j * (j - 1) / 2 - j);
-        else return F + static_cast<int64_t>(j) * k;
+        if (j >= s0) {
+            const int jj = j - s0, nn = k - s0;
+            return sm + (jj * nn - jj * (jj - 1) / 2 - jj - s0);
+        }
+        return F + static_cast<int64_t>(j) * k;
+    };
+    auto move_on_chip = [&](int from) {  // columns >= from: F -> shared memory
+        const int nn = k - from;
+        for (int j = from + wid; j < k; j += nw) {
+            const int jj = j - from;
+            double* dst = sm + (jj * nn - jj * (jj - 1) / 2 - jj - from);
+            const double* src = F + static_cast<int64_t>(j) * k;
+            for (int i = j + lane; i < k; i += 32) dst[i] = src[i];
+        }
+        __syncthreads();
+        s0 = from;
     };
     // (i, j) with i >= j
     auto at = [&](int i, int j) -> double& { return colp(j)[i]; };
@@ -91,6 +109,7 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
     const double alpha = (1.0 + sqrt(17.0)) / 8.0;
     int kk = 0, nb = 0, par = 0;
     while (kk < k) {
+        if (s0 == INT_MAX && kk >= switch_at) move_on_chip(kk);
         double colmax = s_cm[par];
         int imax = s_ci[par];
         if (colmax < 0.0) {
@@ -160,6 +179,7 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
                 double* cj = colp(j);
                 double v = -1.0;
                 int idx = INT_MAX;
+#pragma unroll 4
                 for (int i = j + lane; i < k; i += 32) {
                     const double y = cj[i] - ck[i] * w;
                     cj[i] = y;
@@ -198,6 +218,7 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
                 double* cj = colp(j);
                 double v = -1.0;
                 int idx = INT_MAX;
+#pragma unroll 4
                 for (int i = j + lane; i < k; i += 32) {
                     const double y = cj[i] - (ck[i] * wk + ck1[i] * wk1);
                     cj[i] = y;
@@ -232,8 +253,8 @@ ldlt_bk_kernel(const double* __restrict__ S, int k, double* __restrict__ F, Blk*
         par ^= 1;
     }
     __syncthreads();
-    if (in_smem)
-        for (int j = wid; j < k; j += nw)
+    if (s0 != INT_MAX)
+        for (int j = s0 + wid; j < k; j += nw)
             for (int i = j + lane; i < k; i += 32) F[static_cast<int64_t>(j) * k + i] = at(i, j);
     if (tid == 0) *nblk = nb;
 }
@@ -372,18 +393,23 @@ __global__ void map_cols_kernel(const long long* __restrict__ sampled, const lon
 
 size_t ldlt_scratch_bytes(int k) { return sizeof(Blk) * static_cast<size_t>(k) + 2 * sizeof(int); }
 
+// first step whose trailing triangle fits the shared-memory budget
+static int onchip_switch(int n, size_t cap) {
+    int s0 = 0;
+    while (s0 < n && sizeof(double) * static_cast<size_t>(n - s0) * (n - s0 + 1) / 2 > cap) ++s0;
+    return s0;
+}
+
 cudaError_t ldlt_factor(const double* S, int k, double* F, void* scratch, int* status, cudaStream_t stream) {
     Blk* blocks = static_cast<Blk*>(scratch);
     int* nblk = reinterpret_cast<int*>(blocks + k);
-    const size_t smem = sizeof(double) * static_cast<size_t>(k) * (k + 1) / 2;
-    const bool in_smem = smem <= 220 * 1024;
-    if (in_smem) {
-        cudaError_t e = cudaFuncSetAttribute(ldlt_bk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    if (in_smem) ldlt_bk_kernel<true><<<1, kLdltThreads, smem, stream>>>(S, k, F, blocks, nblk, status);
-    else ldlt_bk_kernel<false><<<1, kLdltThreads, 0, stream>>>(S, k, F, blocks, nblk, status);
+    const size_t cap = 220 * 1024;
+    const int s0 = onchip_switch(k, cap);
+    const size_t smem = sizeof(double) * static_cast<size_t>(k - s0) * (k - s0 + 1) / 2;
+    cudaError_t e = cudaFuncSetAttribute(ldlt_bk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(std::max<size_t>(smem, 1024)));
+    if (e != cudaSuccess) return e;
+    ldlt_bk_kernel<<<1, kLdltThreads, std::max<size_t>(smem, 1024), stream>>>(S, k, F, blocks, nblk, status, s0);
     return cudaGetLastError();
 }
 

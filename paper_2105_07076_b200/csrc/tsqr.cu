@@ -25,16 +25,21 @@ constexpr int kCholThreads = 512;
 // L written into Lf (p x p, ld p; entries above the diagonal zeroed).  Packed
 // by columns in shared memory when it fits, else in place in Lf (L2).
 // *status = index of the first non-positive pivot (untouched on success).
-template <bool kSmem>
 __global__ void __launch_bounds__(kCholThreads)
 cholesky_kernel(const double* __restrict__ G, int p, const double* __restrict__ trace, double shift_factor,
-                double* __restrict__ Lf, int* __restrict__ status) {
+                double* __restrict__ Lf, int* __restrict__ status, int switch_at) {
     extern __shared__ double sm[];
     const double shift = trace ? shift_factor * *trace : 0.0;
     const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = T >> 5;
+    // the working triangle starts in Lf (L2) and moves on chip, packed by
+    // columns, once the trailing part fits (switch_at = 0: from the start)
+    int s0 = INT_MAX;
     auto colp = [&](int j) -> double* {
-        if constexpr (kSmem) return sm + (j * p - j * (j - 1) / 2 - j);
-        else return Lf + static_cast<int64_t>(j) * p;
+        if (j >= s0) {
+            const int jj = j - s0, nn = p - s0;
+            return sm + (jj * nn - jj * (jj - 1) / 2 - jj - s0);
+        }
+        return Lf + static_cast<int64_t>(j) * p;
     };
     for (int j = wid; j < p; j += nw) {
         double* cj = colp(j);
@@ -43,6 +48,17 @@ cholesky_kernel(const double* __restrict__ G, int p, const double* __restrict__ 
     }
     __syncthreads();
     for (int kk = 0; kk < p; ++kk) {
+        if (s0 == INT_MAX && kk >= switch_at) {
+            const int nn = p - kk;
+            for (int j = kk + wid; j < p; j += nw) {
+                const int jj = j - kk;
+                double* dst = sm + (jj * nn - jj * (jj - 1) / 2 - jj - kk);
+                const double* src = Lf + static_cast<int64_t>(j) * p;
+                for (int i = j + lane; i < p; i += 32) dst[i] = src[i];
+            }
+            __syncthreads();
+            s0 = kk;
+        }
         double* ck = colp(kk);
         const double d = ck[kk];
         if (!(d > 0.0)) {
@@ -50,12 +66,13 @@ cholesky_kernel(const double* __restrict__ G, int p, const double* __restrict__ 
             return;
         }
         const double r = sqrt(d);
-        const double inv = 1.0 / r;
+        const double inv = 1.0 / r, invd = 1.0 / d;
         // a(i,j) -= a(i,kk) a(j,kk) / d for kk < j <= i (right-looking, a warp per column)
         for (int j = kk + 1 + wid; j < p; j += nw) {
             double* cj = colp(j);
-            const double w = ck[j] / d;
-            for (int i = j + lane; i < p; i += 32) cj[i] -= ck[i] * w;
+            const double w = ck[j] * invd;
+#pragma unroll 4
+            for (int i = j + lane; i < p; i += 32) cj[i] = fma(-ck[i], w, cj[i]);
         }
         __syncthreads();
         for (int i = kk + 1 + tid; i < p; i += T) ck[i] *= inv;
@@ -65,7 +82,10 @@ cholesky_kernel(const double* __restrict__ G, int p, const double* __restrict__ 
     __syncthreads();
     for (int j = wid; j < p; j += nw) {
         const double* cj = colp(j);
-        for (int i = lane; i < p; i += 32) Lf[static_cast<int64_t>(j) * p + i] = i >= j ? cj[i] : 0.0;
+        for (int i = lane; i < p; i += 32) {
+            const double v = i >= j ? cj[i] : 0.0;
+            Lf[static_cast<int64_t>(j) * p + i] = v;
+        }
     }
 }
 
@@ -145,15 +165,14 @@ size_t cholesky_smem_bytes(int p) { return sizeof(double) * static_cast<size_t>(
 
 cudaError_t cholesky_lower(const double* G, int p, const double* trace, double shift_factor, double* L, int* status,
                            cudaStream_t stream) {
-    const size_t smem = cholesky_smem_bytes(p);
-    if (smem <= 220 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(cholesky_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        cholesky_kernel<true><<<1, kCholThreads, smem, stream>>>(G, p, trace, shift_factor, L, status);
-    } else {
-        cholesky_kernel<false><<<1, kCholThreads, 0, stream>>>(G, p, trace, shift_factor, L, status);
-    }
+    const size_t cap = 220 * 1024;
+    int s0 = 0;
+    while (s0 < p && sizeof(double) * static_cast<size_t>(p - s0) * (p - s0 + 1) / 2 > cap) ++s0;
+    const size_t smem = std::max<size_t>(sizeof(double) * static_cast<size_t>(p - s0) * (p - s0 + 1) / 2, 1024);
+    cudaError_t e = cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cholesky_kernel<<<1, kCholThreads, smem, stream>>>(G, p, trace, shift_factor, L, status, s0);
     return cudaGetLastError();
 }
 
