@@ -115,7 +115,7 @@ def test_invalid_arguments(idk, ref):
         idk.optim_rid(a, 3, -0.5, 1)
 
 
-@pytest.mark.parametrize("m,n", [(16, 16), (40, 12), (300, 90)])
+@pytest.mark.parametrize("m,n", [(16, 16), (40, 12), (300, 90), (3000, 400)])
 def test_id_auto_sampled_vs_reference(idk, ref, m, n):
     """id_auto(randomized) of the reference routes through optim_rid, tall inputs
     through A^T (id.cpp:78-95); method SAMPLED reproduces it, dual included."""
