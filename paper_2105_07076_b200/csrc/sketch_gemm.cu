@@ -314,6 +314,7 @@ __global__ void resid_reduce_kernel(const double* __restrict__ part, int64_t cou
 
 // Pick BM = 16*WM (WM in 2..7) minimising padded rows over ceil(M/BM) tiles.
 int sketch_gemm_pick_wm(int M) {
+    if (const char* e = getenv("IDK_GEMM_WM")) return atoi(e);  // tuning experiments
     int best = 7;
     int64_t best_pad = INT64_MAX;
     for (int wm = 7; wm >= 2; --wm) {
