@@ -51,6 +51,10 @@ struct idk_context {
     std::vector<idk_context*> kids;
     cudaEvent_t ev_fork = nullptr;
     std::vector<cudaEvent_t> ev_join;
+    // grouped sketch of the batch entry: a low-priority stream feeding the lanes
+    cudaStream_t s_sketch = nullptr;
+    std::vector<cudaEvent_t> ev_chunk;   // chunk c's Y ready
+    std::vector<cudaEvent_t> ev_gprof;   // profiling: 3 per chunk (start, Omega done, GEMM done)
     // per-stage CUDA events on the launching stream (idk_set_profiling)
     bool profiling = false;
     cudaEvent_t ev[6] = {};
@@ -568,6 +572,9 @@ int idk_destroy(idk_handle h) {
         cudaStreamDestroy(ks);
     }
     for (cudaEvent_t e : h->ev_join) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->ev_chunk) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->ev_gprof) cudaEventDestroy(e);
+    if (h->s_sketch) cudaStreamDestroy(h->s_sketch);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ws) cudaFree(h->ws);
     if (h->io) cudaFree(h->io);
@@ -990,6 +997,113 @@ int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a,
     return IDK_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Grouped batch of sketch RIDs (idk_id_auto_batch, method 1, Philox Omega):
+// the Omegas and sketches of `chunk` IDs at a time run as ONE Omega launch and
+// ONE grouped DMMA GEMM on a low-priority stream (small sketches fill the GPU
+// together instead of each running a split-K launch at half the DMMA rate),
+// and lane i % L -- a high-priority stream -- factors Y_i (CPQR, Z, C) as soon
+// as its chunk's sketch is done, overlapping the next chunk's GEMM.  Results
+// are those of idk_id_auto on each ID: the grouped GEMM uses the same tile
+// order and fixed split-K order as the single sketch for the same splits.
+int batch_grouped(idk_context* h, int L, int64_t count, const double* const* d_a, int64_t m, int64_t n, int64_t lda,
+                  int64_t k, const uint64_t* seeds, int64_t p, int64_t* const* d_cols, double* const* d_z,
+                  double* const* d_c, int* transposed, int64_t* issued) {
+    if (p < 0) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: oversampling p must be non-negative");
+    if (lda < m) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: lda too small");
+    const bool tall = m > n;
+    if (transposed) *transposed = tall ? 1 : 0;
+    const int64_t mm = tall ? n : m, nn = tall ? m : n;  // M = A or A^T: mm x nn
+    const int64_t l = k + p;
+    for (int64_t i = 0; i < count; ++i)
+        if (!d_a[i] || !d_cols[i] || !d_z[i]) return set_err(h, IDK_ERR_INVALID_ARG, "sketch_rid: null pointer");
+    const CpqrChoice ch = choose_cpqr(h, l, nn, k);
+    int rc = check_cpqr_fits(h, l, nn, ch);
+    if (rc) return rc;
+    int chunk = 4;
+    if (const char* e = getenv("IDK_BATCH_CHUNK")) chunk = std::max(1, atoi(e));
+    chunk = static_cast<int>(std::min<int64_t>({chunk, count, idk::kGemmGroupMax}));
+    // the single sketch's split count, so each Y_i is bit-identical to idk_id_auto's
+    const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(l), nn, mm, h->num_sms);
+    const int64_t nchunks = (count + chunk - 1) / chunk;
+    Carve cv;
+    const size_t oofs = cv.take(sizeof(double) * l * mm * chunk * 2);  // double-buffered by chunk parity
+    const size_t yofs = cv.take(sizeof(double) * l * nn * count);
+    const size_t pofs = splits > 1 ? cv.take(sizeof(double) * l * nn * splits * chunk * 2) : 0;
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    if (!h->s_sketch) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        IDK_CUDA(cudaStreamCreateWithPriority(&h->s_sketch, cudaStreamNonBlocking, lo));
+    }
+    while (static_cast<int64_t>(h->ev_chunk.size()) < nchunks) {
+        cudaEvent_t e;
+        IDK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_chunk.push_back(e);
+    }
+    if (h->profiling) {
+        while (static_cast<int64_t>(h->ev_gprof.size()) < 3 * nchunks) {
+            cudaEvent_t e;
+            IDK_CUDA(cudaEventCreate(&e));
+            h->ev_gprof.push_back(e);
+        }
+    }
+    IDK_CUDA(cudaStreamWaitEvent(h->s_sketch, h->ev_fork, 0));
+    double* Ybase = reinterpret_cast<double*>(h->ws + yofs);
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t i0 = c * chunk;
+        const int cnt = static_cast<int>(std::min<int64_t>(chunk, count - i0));
+        double* om = reinterpret_cast<double*>(h->ws + oofs) + (c & 1) * l * mm * chunk;
+        double* part = splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) + (c & 1) * l * nn * splits * chunk
+                                  : nullptr;
+        // Omega / partial buffers are double-buffered: chunk c reuses chunk c-2's, which
+        // the stream order already finished (the GEMM of c-2 precedes this launch)
+        idk::GroupSeeds sd{};
+        idk::GemmGroup g{};
+        g.count = cnt;
+        g.a_stride = l * mm;
+        for (int t = 0; t < cnt; ++t) {
+            sd.s[t] = seeds ? seeds[i0 + t] : 0;
+            g.b[t] = d_a[i0 + t];
+            g.y[t] = Ybase + (i0 + t) * l * nn;
+        }
+        if (h->profiling) IDK_CUDA(cudaEventRecord(h->ev_gprof[3 * c], h->s_sketch));
+        IDK_CUDA(idk::omega_philox_group(om, l, mm, sd, cnt, h->s_sketch));
+        if (h->profiling) IDK_CUDA(cudaEventRecord(h->ev_gprof[3 * c + 1], h->s_sketch));
+        IDK_CUDA(idk::sketch_gemm_group(om, lda, tall, g, l, static_cast<int>(l), nn, mm, splits, part,
+                                        h->s_sketch));
+        if (h->profiling) IDK_CUDA(cudaEventRecord(h->ev_gprof[3 * c + 2], h->s_sketch));
+        IDK_CUDA(cudaEventRecord(h->ev_chunk[static_cast<size_t>(c)], h->s_sketch));
+        h->launches += splits > 1 ? 3 : 2;
+        for (int t = 0; t < cnt; ++t) {
+            const int64_t i = i0 + t;
+            idk_context* kid = h->kids[static_cast<size_t>(i % L)];
+            IDK_CUDA(cudaStreamWaitEvent(kid->stream, h->ev_chunk[static_cast<size_t>(c)], 0));
+            Carve kc;
+            const CpqrWs w = carve_cpqr(kc, l, nn, k, kid->num_sms, ch);
+            if ((rc = ensure(kid, &kid->ws, &kid->ws_cap, kc.total)))
+                return set_err(h, rc, "id_auto_batch: matrix " + std::to_string(i) + ": " + kid->err);
+            h->h_status_many[i] = 0x7f7f7f7f;
+            kid->async_status = h->h_status_many + i;
+            mark(kid, 0);
+            mark(kid, 1);
+            rc = factor_and_solve(kid, ch, g.y[t], l, nn, k, kid->ws, w, d_a[i], lda, mm, tall, d_cols[i], d_z[i],
+                                  d_c ? d_c[i] : nullptr, false);
+            kid->async_status = nullptr;
+            if (rc) return set_err(h, rc, "id_auto_batch: matrix " + std::to_string(i) + ": " + kid->err);
+            ++*issued;
+        }
+    }
+    return IDK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int idk_set_concurrency(idk_handle h, int lanes) {
     if (!h || lanes < 1 || lanes > 64) return IDK_ERR_INVALID_ARG;
     h->lanes = lanes;
@@ -1014,7 +1128,13 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
         idk_context* kid = nullptr;
         if ((rc = idk_create(&kid, h->device))) return set_err(h, rc, "id_auto_batch: lane context creation failed");
         cudaStream_t ks;
-        if (cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking) != cudaSuccess) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        const char* pe = getenv("IDK_LANE_PRIO");
+        if (pe && atoi(pe) == 0) hi = 0;
+        // lanes run the latency-bound CPQRs: highest priority, so their clusters
+        // are dispatched ahead of the (low-priority) grouped sketch CTAs
+        if (cudaStreamCreateWithPriority(&ks, cudaStreamNonBlocking, hi) != cudaSuccess) {
             idk_destroy(kid);
             return set_err(h, IDK_ERR_CUDA, "id_auto_batch: stream creation failed");
         }
@@ -1048,7 +1168,16 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
     int first_rc = IDK_OK;
     int64_t issued = 0;
     const auto t_enqueue0 = std::chrono::steady_clock::now();
-    for (int64_t i = 0; i < count && first_rc == IDK_OK; ++i, ++issued) {
+    const char* ge = getenv("IDK_BATCH_GROUPED");
+    // opt-in (IDK_BATCH_GROUPED=1): measured at cfg2 with 16 IDs it ties the per-lane
+    // schedule (5681 vs 5632 IDs/s at chunk 4) -- the CPQR clusters (at most 7
+    // co-resident 16-CTA clusters, profiles/probe_clusters_r01.txt) bound both
+    const bool grouped = method == 1 && omega_mode == IDK_OMEGA_PHILOX && count >= 2 && ge && atoi(ge) == 1;
+    if (grouped) {
+        rc = batch_grouped(h, L, count, d_a, m, n, lda, k, seeds, p, d_cols, d_z, d_c, transposed, &issued);
+        if (rc) first_rc = rc;
+    }
+    for (int64_t i = 0; !grouped && i < count && first_rc == IDK_OK; ++i, ++issued) {
         idk_context* kid = h->kids[static_cast<size_t>(i % L)];
         h->h_status_many[i] = 0x7f7f7f7f;
         kid->async_status = h->h_status_many + i;
@@ -1077,6 +1206,20 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
             idk_context* kid = h->kids[static_cast<size_t>(l)];
             collect_stage_times(kid);
             for (int j = 0; j < 5; ++j) h->stage_ms[j] += kid->stage_ms[j] / static_cast<float>(L);
+        }
+        if (grouped && issued > 0) {  // Omega / sketch: the grouped launches' device time per ID
+            float om = 0.f, gm = 0.f;
+            const size_t chunks = h->ev_gprof.size() / 3;
+            for (size_t c = 0; c < chunks; ++c) {
+                float a = 0.f, b = 0.f;
+                if (cudaEventElapsedTime(&a, h->ev_gprof[3 * c], h->ev_gprof[3 * c + 1]) != cudaSuccess) a = 0.f;
+                if (cudaEventElapsedTime(&b, h->ev_gprof[3 * c + 1], h->ev_gprof[3 * c + 2]) != cudaSuccess) b = 0.f;
+                cudaGetLastError();
+                om += a;
+                gm += b;
+            }
+            h->stage_ms[0] = om / static_cast<float>(issued);
+            h->stage_ms[1] = gm / static_cast<float>(issued);
         }
     }
     if (first_rc) return first_rc;

@@ -8,6 +8,20 @@
 namespace idk {
 
 // sketch_gemm.cu
+constexpr int kGemmGroupMax = 32;
+struct GemmGroup {  // grouped sketch members (kernel parameter, by value)
+    int count = 0, splits = 1;
+    int64_t a_stride = 0, c_stride = 0;
+    const double* b[kGemmGroupMax];
+    double* y[kGemmGroupMax];
+};
+struct GroupSeeds {
+    uint64_t s[kGemmGroupMax];
+};
+cudaError_t sketch_gemm_group(const double* omega, int64_t ldb, bool b_trans, const GemmGroup& grp, int64_t ldc,
+                              int M, int64_t N, int64_t K, int splits, double* partial, cudaStream_t stream);
+cudaError_t omega_philox_group(double* out, int64_t l, int64_t m, const GroupSeeds& seeds, int count,
+                               cudaStream_t stream);
 int sketch_gemm_pick_wm(int M);
 int sketch_gemm_pick_splits(int M, int64_t N, int64_t K, int num_sms);
 cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans, double* Y,

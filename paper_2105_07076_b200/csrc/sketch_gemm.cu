@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "kernels.h"
 
 namespace idk {
 
@@ -67,7 +68,8 @@ sketch_gemm_kernel(const double* __restrict__ A, int64_t lda,  // Omega: l x K
                    double* __restrict__ C, int64_t ldc,        // Y (or split-K partial base)
                    int64_t split_stride,                       // elements between split partials
                    int M, int64_t N, int64_t K, int64_t k_per_split, bool vec16,
-                   const double* __restrict__ Ref, int64_t ldr, bool ref_trans, double* __restrict__ resid) {
+                   const double* __restrict__ Ref, int64_t ldr, bool ref_trans, double* __restrict__ resid,
+                   const GemmGroup grp) {
     using S = Smem<WM, kNT>;
     constexpr int BM = S::BM;
     extern __shared__ __align__(16) double smem[];
@@ -76,10 +78,18 @@ sketch_gemm_kernel(const double* __restrict__ A, int64_t lda,  // Omega: l x K
     const int wm = warp & 1, wn = warp >> 1;
     const int m0 = blockIdx.x * BM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.y) * kBN;
-    const int64_t kbeg = static_cast<int64_t>(blockIdx.z) * k_per_split;
+    int split = blockIdx.z;
+    if (grp.count > 0) {  // grouped launch: blockIdx.z = member * splits + split
+        const int g = blockIdx.z / grp.splits;
+        split = blockIdx.z - g * grp.splits;
+        A += g * grp.a_stride;
+        B = grp.b[g];
+        C += g * grp.c_stride;
+    }
+    const int64_t kbeg = static_cast<int64_t>(split) * k_per_split;
     const int64_t kend = min(K, kbeg + k_per_split);
     const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBK - 1) / kBK) : 0;
-    C += static_cast<int64_t>(blockIdx.z) * split_stride;
+    C += static_cast<int64_t>(split) * split_stride;
 
     auto load_stage = [&](int stage, int kt) {
         double* As = smem + stage * S::STAGE;
@@ -250,11 +260,30 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ P, int64_t split
     }
 }
 
+// Grouped form: member g reduces the partials at P + g*group_stride into Ys[g].
+__global__ void splitk_reduce_group_kernel(const double* __restrict__ P, int64_t split_stride, int splits,
+                                           int64_t group_stride, const GemmGroup grp, int M, int64_t N,
+                                           int64_t ldc) {
+    const int64_t total = static_cast<int64_t>(M) * N;
+    const int g = blockIdx.y;
+    P += g * group_stride;
+    double* Y = grp.y[g];
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / M;
+        const int i = static_cast<int>(e - j * M);
+        const int64_t off = j * ldc + i;
+        double s = P[off];
+        for (int t = 1; t < splits; ++t) s += P[t * split_stride + off];
+        Y[off] = s;
+    }
+}
+
 template <int WM, bool kNT>
 cudaError_t launch_wm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K, int splits,
                       bool vec16, cudaStream_t stream, const double* Ref = nullptr, int64_t ldr = 0,
-                      bool ref_trans = false, double* resid = nullptr) {
+                      bool ref_trans = false, double* resid = nullptr, const GemmGroup* grp = nullptr) {
     using S = Smem<WM, kNT>;
     auto kern = sketch_gemm_kernel<WM, kNT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -262,24 +291,31 @@ cudaError_t launch_wm(const double* A, int64_t lda, const double* B, int64_t ldb
     if (e != cudaSuccess) return e;
     int64_t kps = (K + splits - 1) / splits;
     kps = ((kps + kBK - 1) / kBK) * kBK;
-    dim3 grid((M + S::BM - 1) / S::BM, static_cast<unsigned>((N + kBN - 1) / kBN), splits);
+    GemmGroup g{};
+    if (grp) g = *grp;
+    g.splits = splits;
+    const unsigned gz = static_cast<unsigned>(splits * (g.count > 0 ? g.count : 1));
+    dim3 grid((M + S::BM - 1) / S::BM, static_cast<unsigned>((N + kBN - 1) / kBN), gz);
     kern<<<grid, kThreads, S::BYTES, stream>>>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, kps,
-                                               vec16, Ref, ldr, ref_trans, resid);
+                                               vec16, Ref, ldr, ref_trans, resid, g);
     return cudaGetLastError();
 }
 
 template <bool kNT>
 cudaError_t launch_nt(int wm, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K, int splits,
-                      bool vec16, cudaStream_t stream) {
+                      bool vec16, cudaStream_t stream, const GemmGroup* grp = nullptr) {
+#define IDK_LWM(W) launch_wm<W, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream, \
+                                     nullptr, 0, false, nullptr, grp)
     switch (wm) {
-        case 2: return launch_wm<2, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
-        case 3: return launch_wm<3, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
-        case 4: return launch_wm<4, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
-        case 5: return launch_wm<5, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
-        case 6: return launch_wm<6, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
-        default: return launch_wm<7, kNT>(A, lda, B, ldb, C, ldc, split_stride, M, N, K, splits, vec16, stream);
+        case 2: return IDK_LWM(2);
+        case 3: return IDK_LWM(3);
+        case 4: return IDK_LWM(4);
+        case 5: return IDK_LWM(5);
+        case 6: return IDK_LWM(6);
+        default: return IDK_LWM(7);
     }
+#undef IDK_LWM
 }
 
 }  // namespace
@@ -363,6 +399,49 @@ cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t l
     return cudaGetLastError();
 }
 
+// Grouped sketch: Y_g = Omega_g * op(B_g) for g < grp.count, Omega_g at
+// omega + g*grp.a_stride (ld = M), B_g = grp.b[g], Y_g = grp.y[g] (ld = ldc).
+// One launch over every member (blockIdx.z = member * splits + split) so small
+// sketches fill the GPU together; split-K partials (splits > 1) live at
+// partial + (g*splits + s) * ldc*N and are reduced in the same fixed order as
+// sketch_gemm, so a member's Y is bit-identical to its single launch with the
+// same splits.
+cudaError_t sketch_gemm_group(const double* omega, int64_t ldb, bool b_trans, const GemmGroup& grp, int64_t ldc,
+                              int M, int64_t N, int64_t K, int splits, double* partial, cudaStream_t stream) {
+    if (M <= 0 || N <= 0 || grp.count <= 0) return cudaSuccess;
+    if (grp.count > kGemmGroupMax) return cudaErrorInvalidValue;
+    const int wm = sketch_gemm_pick_wm(M);
+    bool vec16 = (M % 2 == 0) && (ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(omega) & 15) == 0) &&
+                 ((grp.a_stride % 2) == 0);
+    for (int g = 0; g < grp.count; ++g) vec16 = vec16 && ((reinterpret_cast<uintptr_t>(grp.b[g]) & 15) == 0);
+    if (splits < 1) splits = 1;
+    const int64_t split_stride = ldc * N;
+    GemmGroup g = grp;
+    // The kernel addresses C as base + g*c_stride: with splits == 1 it writes Y_g
+    // directly when the Y_g are equally spaced; otherwise it goes through partials.
+    bool spaced = splits == 1;
+    for (int t = 1; spaced && t < grp.count; ++t) spaced = grp.y[t] - grp.y[0] == t * (grp.y[1] - grp.y[0]);
+    double* out;
+    if (spaced) {
+        out = grp.y[0];
+        g.c_stride = grp.count > 1 ? grp.y[1] - grp.y[0] : 0;
+    } else {
+        if (!partial) return cudaErrorInvalidValue;
+        out = partial;
+        g.c_stride = split_stride * splits;
+    }
+    cudaError_t e = b_trans ? launch_nt<true>(wm, omega, M, nullptr, ldb, out, ldc, split_stride, M, N, K, splits,
+                                              vec16, stream, &g)
+                            : launch_nt<false>(wm, omega, M, nullptr, ldb, out, ldc, split_stride, M, N, K, splits,
+                                               vec16, stream, &g);
+    if (e != cudaSuccess || spaced) return e;
+    const int64_t total = static_cast<int64_t>(M) * N;
+    const int bx = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16 / grp.count + 1));
+    splitk_reduce_group_kernel<<<dim3(bx, grp.count), 256, 0, stream>>>(partial, split_stride, splits,
+                                                                       split_stride * splits, grp, M, N, ldc);
+    return cudaGetLastError();
+}
+
 // Residual of a product: out2 = {||Ref - A*B||_F^2, ||Ref||_F^2} with A (M x K,
 // lda) and B (K x N, ldb); Ref is M x N (ldr) or, with ref_trans, N x M.
 // `part` needs resid_partials(M, N) doubles.
@@ -404,7 +483,26 @@ __global__ void omega_philox_kernel(double* __restrict__ out, int64_t total, uin
          e += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[e] = philox_normal(static_cast<uint64_t>(e), seed);
 }
+
+// One Omega per group member (blockIdx.y), member g at out + g*total.
+__global__ void omega_philox_group_kernel(double* __restrict__ out, int64_t total, const GroupSeeds seeds) {
+    const uint64_t seed = seeds.s[blockIdx.y];
+    out += blockIdx.y * total;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[e] = philox_normal(static_cast<uint64_t>(e), seed);
+}
 }  // namespace
+
+cudaError_t omega_philox_group(double* out, int64_t l, int64_t m, const GroupSeeds& seeds, int count,
+                               cudaStream_t stream) {
+    const int64_t total = l * m;
+    if (total <= 0 || count <= 0) return cudaSuccess;
+    if (count > kGemmGroupMax) return cudaErrorInvalidValue;
+    const int bx = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8 / count + 1));
+    omega_philox_group_kernel<<<dim3(bx, count), 256, 0, stream>>>(out, total, seeds);
+    return cudaGetLastError();
+}
 
 cudaError_t omega_philox(double* out, int64_t l, int64_t m, uint64_t seed, cudaStream_t stream) {
     const int64_t total = l * m;

@@ -371,3 +371,22 @@ def test_diagnostics_and_approx_match_reference(idk, ref, shape, k, method):
     else:
         want = a[:, cols] @ z
     assert rel(ap, want) <= 1e-13
+
+
+@pytest.mark.parametrize("chunk,grouped", [("1", "1"), ("3", "1"), ("32", "1"), ("4", "0"), ("4", "")])
+def test_grouped_sketch_batch_matches_single_calls(idk, oracle, monkeypatch, chunk, grouped):
+    """The grouped sketch path of idk_id_auto_batch (one Omega launch + one DMMA
+    GEMM per chunk of IDs on a low-priority stream, CPQR on the lanes) is
+    bit-identical to single idk_id_auto calls for any chunk size, tall or wide."""
+    monkeypatch.setenv("IDK_BATCH_CHUNK", chunk)
+    monkeypatch.setenv("IDK_BATCH_GROUPED", grouped)
+    for shape, k in (((110, 2100), 30), ((700, 90), 12)):
+        mats = [dev(oracle.gaussian_matrix(shape[0], shape[1], 70 + s)) for s in range(7)]
+        seeds = [300 + s for s in range(7)]
+        cols, zs, cs, tr = idk.id_auto_batch(mats, k, idk.RANDOMIZED, seeds=seeds, p=6, lanes=3)
+        assert tr == (shape[0] > shape[1])
+        for x, sd, c_, z_, cc in zip(mats, seeds, cols, zs, cs):
+            r = idk.id_auto(x, k, idk.RANDOMIZED, seed=sd, p=6)
+            assert np.array_equal(host(c_), host(r.cols))
+            assert np.array_equal(host(z_), host(r.z))
+            assert np.array_equal(host(cc), host(r.c))
