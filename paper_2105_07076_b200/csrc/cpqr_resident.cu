@@ -142,6 +142,27 @@ __device__ __forceinline__ void reflector(double alpha, double tail, int len, do
     }
 }
 
+// reflector() evaluated by a whole warp: the two divisions run side by side
+// in lanes 0 and 1 (one SIMT division instead of two dependent ones); every
+// lane returns the same, exactly rounded tau, beta, scale.
+__device__ __forceinline__ void reflector_warp(double alpha, double tail, int len, double& tau, double& beta,
+                                               double& scale) {
+    tau = 0.0;
+    beta = alpha;
+    scale = 1.0;
+    if (len > 1 && tail != 0.0) {
+        beta = -copysign(sqrt(add_rn(mul_rn(alpha, alpha), tail)), alpha);
+        const unsigned lane = threadIdx.x & 31u;
+        const double num = lane == 0 ? beta - alpha : 1.0;
+        const double den = lane == 0 ? beta : alpha - beta;
+        const double qd = num / den;
+        tau = __shfl_sync(0xffffffffu, qd, 0);
+        scale = __shfl_sync(0xffffffffu, qd, 1);
+    }
+}
+
+constexpr int kPubRegs = 4;  // candidate rows per lane kept in registers (m - first <= 128)
+
 __device__ __forceinline__ unsigned long long tagged(unsigned payload, unsigned tag) {
     return (static_cast<unsigned long long>(payload) << 32) | tag;
 }
@@ -512,20 +533,71 @@ cpqr_resident_kernel(ResidentArgs a) {
                     }
                 }
                 __syncwarp();
+                trace_by(lane == 0, step, 8);
                 const double* wrow = rows + static_cast<size_t>(winlc) * lds;
                 double al = 0.0, tl = 0.0;
-                for (int i = first + lane; i < m; i += 32) {
-                    const double y = fma(-ww, xa[i], i < l0 ? wrow[i] : xbuf[i]);  // == the group's own axpy
-                    xbuf[i] = y;
-                    if (i == first) al = y;
-                    else tl = fma(y, y, tl);
-                }
-                al = __shfl_sync(kFull, al, 0);  // row `first` is lane 0's first row
-                tl = warp_sum(tl);
                 double tu, be, sc;
-                reflector(al, tl, m - first, tu, be, sc);
-                for (int i = first + lane; i < m; i += 32)
-                    own[i] = tu != 0.0 ? (i == first ? 1.0 : mul_rn(xbuf[i], sc)) : xbuf[i];
+                if (m - first <= 32 * kPubRegs) {
+                    // the updated rows stay in registers (kPubRegs per lane) between
+                    // the norm and the scaled write
+                    double yv[kPubRegs];
+#pragma unroll
+                    for (int t = 0; t < kPubRegs; ++t) {
+                        const int i = first + lane + 32 * t;
+                        yv[t] = 0.0;
+                        if (i < m) {
+                            const double y = fma(-ww, xa[i], i < l0 ? wrow[i] : xbuf[i]);  // == the group's own axpy
+                            yv[t] = y;
+                            if (i == first) al = y;
+                            else tl = fma(y, y, tl);
+                        }
+                    }
+                    al = __shfl_sync(kFull, al, 0);  // row `first` is lane 0's first row
+                    tl = warp_sum(tl);
+                    trace_by(lane == 0, step, 9);
+                    reflector_warp(al, tl, m - first, tu, be, sc);
+                    trace_by(lane == 0, step, 10);
+#pragma unroll
+                    for (int t = 0; t < kPubRegs; ++t) {
+                        const int i = first + lane + 32 * t;
+                        if (i < m) own[i] = tu != 0.0 ? (i == first ? 1.0 : mul_rn(yv[t], sc)) : yv[t];
+                    }
+                } else {
+                    // tall candidates (pull mode): kPubRegs rows per lane per batch,
+                    // all loads of a batch issued before its stores
+                    for (int i0 = first + lane; i0 < m; i0 += 32 * kPubRegs) {
+                        double yv[kPubRegs];
+#pragma unroll
+                        for (int t = 0; t < kPubRegs; ++t) {
+                            const int i = i0 + 32 * t;
+                            yv[t] = i < m ? fma(-ww, xa[i], i < l0 ? wrow[i] : xbuf[i]) : 0.0;  // the group's axpy
+                        }
+#pragma unroll
+                        for (int t = 0; t < kPubRegs; ++t) {
+                            const int i = i0 + 32 * t;
+                            if (i < m) {
+                                xbuf[i] = yv[t];
+                                if (i == first) al = yv[t];
+                                else tl = fma(yv[t], yv[t], tl);
+                            }
+                        }
+                    }
+                    al = __shfl_sync(kFull, al, 0);
+                    tl = warp_sum(tl);
+                    trace_by(lane == 0, step, 9);
+                    reflector_warp(al, tl, m - first, tu, be, sc);
+                    trace_by(lane == 0, step, 10);
+                    for (int i0 = first + lane; i0 < m; i0 += 32 * kPubRegs) {
+                        double yv[kPubRegs];
+#pragma unroll
+                        for (int t = 0; t < kPubRegs; ++t) yv[t] = i0 + 32 * t < m ? xbuf[i0 + 32 * t] : 0.0;
+#pragma unroll
+                        for (int t = 0; t < kPubRegs; ++t) {
+                            const int i = i0 + 32 * t;
+                            if (i < m) own[i] = tu != 0.0 ? (i == first ? 1.0 : mul_rn(yv[t], sc)) : yv[t];
+                        }
+                    }
+                }
                 if (lane == 0) {
                     hd[0] = __longlong_as_double(c0 + winlc);
                     hd[1] = tu;
@@ -533,8 +605,8 @@ cpqr_resident_kernel(ResidentArgs a) {
                     hd[3] = sc;
                 }
             }
+            if (lane < first - lo) own[lo + lane] = 0.0;  // retired rows read v = 0
             if (lane == 0) {
-                for (int i = lo; i < first; ++i) own[i] = 0.0;  // retired rows read v = 0
                 hd[4] = have ? mx : -1.0;
                 hd[5] = __longlong_as_double(have ? static_cast<long long>(winpos) : 0xffffffffLL);
                 if (!push) {
@@ -542,8 +614,10 @@ cpqr_resident_kernel(ResidentArgs a) {
                     for (int j = 0; j < kCHdr; ++j) mine[j] = hd[j];
                 }
             }
+            trace_by(lane == 0, step, 11);
             fence_proxy_async_smem();  // staging writes (generic proxy) -> bulk-copy reads (async proxy)
             __syncwarp();
+            trace_by(lane == 0, step, 12);
             // the arrive releases the local staging to this CTA's waiters; the
             // peers' copies complete the transaction count
             if (lane == 0) mbar_expect_tx(mb, static_cast<unsigned>(G - 1) * bytes);
@@ -783,6 +857,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                     }
                 }
                 __syncwarp();
+                trace_by(lane == 0, step, 8);
                 const double* wrow = rows + static_cast<size_t>(winlc) * lds;
                 double al = 0.0, tl = 0.0;
                 for (int i = first + lane; i < m; i += 32) {

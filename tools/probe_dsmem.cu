@@ -11,6 +11,9 @@
 //   6 warp 0: st.shared::cluster header + remote mbarrier arrive (release.cluster); all wait (acquire.cluster)
 //   7 variant 6 + ld.shared::cluster winner rows + __syncthreads
 //   8 warp 0: bulk push hdr+rows 1/peer (mbarrier tx), all wait (the kernel's push mode)
+//   9 15 warps issue one bulk push each
+//  10 warp 0: st.async 16-B remote stores of hdr+rows to every peer (mbarrier tx)
+//  11 warps 0..14: warp w st.async's hdr+rows to peer w (mbarrier tx)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/probe_dsmem tools/probe_dsmem.cu
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -45,6 +48,11 @@ __device__ __forceinline__ void mbar_arrive_remote(unsigned a_cluster) {
 }
 __device__ __forceinline__ void st_cluster_v2(unsigned a, double x, double y) {
     asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(unsigned a, double x, double y, unsigned mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(a), "d"(x),
+                 "d"(y), "r"(mbar)
+                 : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cl(unsigned a, unsigned par) {
     asm volatile(
@@ -171,6 +179,23 @@ __global__ void __cluster_dims__(G, 1, 1) probe(int variant, int rows, int round
             }
             mbar_wait(mb, (phase >> p) & 1u);
             phase ^= 1u << p;
+        } else if (variant == 10 || variant == 11) {
+            const unsigned mb = smem_u32(&mbar[p]);
+            const int per = HDR + rows, nch = per / 2;
+            if (tid == 0) mbar_expect_tx(mb, (G - 1) * per * 8);
+            const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+            if (variant == 10 && w == 0) {
+                for (int e = ln; e < (G - 1) * nch; e += 32) {
+                    const int gi = e / nch, c = e - gi * nch, g = gi < me ? gi : gi + 1;
+                    st_async_v2(mapa_u32(smem_u32(own + 2 * c), g), own[2 * c], own[2 * c + 1], mapa_u32(mb, g));
+                }
+            } else if (variant == 11 && w < G - 1) {
+                const int g = w < me ? w : w + 1;
+                const unsigned rb = mapa_u32(smem_u32(own), g), rm = mapa_u32(mb, g);
+                for (int c = ln; c < nch; c += 32) st_async_v2(rb + 16 * c, own[2 * c], own[2 * c + 1], rm);
+            }
+            mbar_wait(mb, (phase >> p) & 1u);
+            phase ^= 1u << p;
         } else if (variant == 3) {
             if (tid < G && tid != me) {
                 double* dst = cl.map_shared_rank(own, tid);
@@ -205,9 +230,9 @@ int main() {
                            "st.cluster hdr + cluster.sync + ld.cluster rows", "st.cluster hdr+rows + cluster.sync",
                            "bulk push hdr + mbar + ld.cluster rows", "warp0 st.cluster hdr + remote arrive",
                            "warp0 st.cluster hdr + remote arrive + ld.cluster rows", "warp0 bulk push 1/peer + mbar",
-                           "15 warps x 1 bulk push + mbar"};
+                           "15 warps x 1 bulk push + mbar", "warp0 st.async hdr+rows to all peers", "warp w st.async hdr+rows to peer w"};
     for (int rows : {112, 272, 512}) {
-        for (int v = 0; v < 10; ++v) {
+        for (int v = 0; v < 12; ++v) {
             const size_t smem = sizeof(double) * 2 * G * (HDR + rows);
             cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

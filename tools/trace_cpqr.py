@@ -55,6 +55,12 @@ print(f"step (cta0): mean {tot.mean():.0f} ns  first {tot[0]:.0f}  last {tot[-1]
 if t[:, :steps, 7].max() > 0:
     d = t[:, :steps, 7] - t[:, :steps, 2]
     print(f"{'(tid0 deferred axpy)':24s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+if t[:, :steps, 8].max() > 0:  # cluster publish path of the winner warp (marks 2 -> 8..12 -> 3)
+    pw = [("winner rows staged", 2, 8), ("pending update + norm", 8, 9), ("reflector scalars", 9, 10),
+          ("scaled v + header", 10, 11), ("fence.proxy.async", 11, 12), ("bulk pushes issued", 12, 3)]
+    for nm, a0, a1 in pw:
+        d = t[:, :steps, a1] - t[:, :steps, a0]
+        print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
 for lo, hi in [(0, 10), (k // 2 - 5, k // 2 + 5), (steps - 10, steps)]:
     dd = [(t[:, lo:hi, i + 1] - t[:, lo:hi, i]).mean() for i in range(6)]
     print(f"  steps {lo:3d}-{hi:3d}: " + " ".join(f"{x:7.0f}" for x in dd))
