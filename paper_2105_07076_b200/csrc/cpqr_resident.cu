@@ -415,15 +415,12 @@ cpqr_resident_kernel(ResidentArgs a) {
             const int i = q + S * r;
             myrows[i] = fma(-w, pxa[i], myrows[i]);
         }
-        switch (prr0) {
-#define IDK_AXPY_CASE(r)                                         \
-    case r:                                                      \
-        if constexpr (r < R) yr[r] = fma(-w, xr[S * r], yr[r]);  \
-        [[fallthrough]];
-            IDK_REP32(IDK_AXPY_CASE)
-#undef IDK_AXPY_CASE
-            default:
-                break;
+        // straight-line over every register row (all reflector loads in flight
+        // at once); retired rows keep their value bit for bit through a select
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double nv = fma(-w, xr[S * r], yr[r]);
+            yr[r] = r >= prr0 ? nv : yr[r];
         }
     };
 
@@ -967,6 +964,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             if (tau != 0.0) {
                 double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
                 int r = sr0;
+#pragma unroll 2
                 for (; r + 4 <= nsr; r += 4) {
                     const int i = q + S * r;
                     const double y0 = myrows[i], y1 = myrows[i + S], y2 = myrows[i + 2 * S], y3 = myrows[i + 3 * S];
@@ -980,20 +978,17 @@ cpqr_resident_kernel(ResidentArgs a) {
                     const int i = q + S * r;
                     d0 = fma(xa[i], myrows[i], d0);
                 }
-                switch (rr0) {
-#define IDK_DOT_CASE(r)                                                     \
-    case r:                                                                 \
-        if constexpr (r < R) {                                              \
-            if ((r & 3) == 0) d0 = fma(xr[S * r], yr[r], d0);               \
-            else if ((r & 3) == 1) d1 = fma(xr[S * r], yr[r], d1);          \
-            else if ((r & 3) == 2) d2 = fma(xr[S * r], yr[r], d2);          \
-            else d3 = fma(xr[S * r], yr[r], d3);                            \
-        }                                                                   \
-        [[fallthrough]];
-                    IDK_REP32(IDK_DOT_CASE)
-#undef IDK_DOT_CASE
-                    default:
-                        break;
+                // Every register row, retired ones included: v is zero above row s
+                // (absolute-row addressing), so the extra terms add exact zeros, and
+                // one straight-line block lets all R reflector loads issue back to
+                // back instead of one load-use round trip per row.
+#pragma unroll
+                for (int r = 0; r < R; r += 4) {
+                    const double v0 = xr[S * r], v1 = xr[S * (r + 1)], v2 = xr[S * (r + 2)], v3 = xr[S * (r + 3)];
+                    d0 = fma(v0, yr[r], d0);
+                    d1 = fma(v1, yr[r + 1], d1);
+                    d2 = fma(v2, yr[r + 2], d2);
+                    d3 = fma(v3, yr[r + 3], d3);
                 }
                 const double w = mul_rn(group_sum<S>((d0 + d1) + (d2 + d3)), tau);
                 wpend = w;
