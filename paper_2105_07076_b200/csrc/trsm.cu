@@ -257,6 +257,53 @@ __global__ void gather_columns_kernel(const double* __restrict__ A, int64_t lda,
     }
 }
 
+// C[:, j] = A[:, cols[j]] (matrix.cpp:121-130): blockIdx.y = j, each thread
+// moves kGatherVec 16-byte pairs with streaming loads/stores (both columns
+// 16-byte aligned: A, C aligned, lda and rows even).
+constexpr int kGatherVec = 4;
+__global__ void gather_columns_vec_kernel(const double* __restrict__ A, int64_t lda, int64_t rows,
+                                          const long long* __restrict__ cols, double* __restrict__ C) {
+    const int j = blockIdx.y;
+    const double2* src = reinterpret_cast<const double2*>(A + cols[j] * lda);
+    double2* dst = reinterpret_cast<double2*>(C + j * rows);
+    const int64_t pairs = rows >> 1;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * kGatherVec + threadIdx.x;
+    double2 v[kGatherVec];
+#pragma unroll
+    for (int u = 0; u < kGatherVec; ++u) {
+        const int64_t p = base + static_cast<int64_t>(u) * blockDim.x;
+        if (p < pairs) v[u] = __ldcs(src + p);
+    }
+#pragma unroll
+    for (int u = 0; u < kGatherVec; ++u) {
+        const int64_t p = base + static_cast<int64_t>(u) * blockDim.x;
+        if (p < pairs) __stcs(dst + p, v[u]);
+    }
+}
+
+// Rows of A for the dual (id.cpp:85-92): C[i, j] = A[cols[j], i], C is n x k.
+// A CTA takes 32 values of i: warp w reads A[cols[j], i0 + lane] for its j's
+// (32 consecutive i of one row: 32 strided sectors), stages a 32 x k tile in
+// shared memory, and writes C coalesced along i.
+__global__ void gather_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t n,
+                                   const long long* __restrict__ cols, int k, double* __restrict__ C) {
+    extern __shared__ double tile[];  // k x 33
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int64_t i = i0 + lane;
+    int j = wid;
+    for (; j + 3 * nw < k; j += 4 * nw) {  // four independent sector reads in flight per thread
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = i < n ? __ldcs(A + cols[j + u * nw] + i * lda) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tile[(j + u * nw) * 33 + lane] = v[u];
+    }
+    for (; j < k; j += nw) tile[j * 33 + lane] = i < n ? __ldcs(A + cols[j] + i * lda) : 0.0;
+    __syncthreads();
+    for (int j = wid; j < k; j += nw)
+        if (i < n) __stcs(C + static_cast<int64_t>(j) * n + i, tile[j * 33 + lane]);
+}
 __global__ void copy_pivots_kernel(const long long* __restrict__ src, int k, long long* __restrict__ dst) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
@@ -330,6 +377,24 @@ cudaError_t gather_columns(const double* A, int64_t lda, int64_t rows, const lon
                            bool rows_of_a, double* C, cudaStream_t stream) {
     const int64_t total = rows * k;
     if (total <= 0) return cudaSuccess;
+    if (!rows_of_a && rows % 2 == 0 && lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(C) & 15) == 0 && k <= 65535) {
+        const int64_t per = 256LL * kGatherVec;  // pairs per CTA
+        const dim3 grid(static_cast<unsigned>((rows / 2 + per - 1) / per), static_cast<unsigned>(k));
+        gather_columns_vec_kernel<<<grid, 256, 0, stream>>>(A, lda, rows, cols, C);
+        return cudaGetLastError();
+    }
+    if (rows_of_a && sizeof(double) * static_cast<size_t>(k) * 33 <= 200 * 1024) {
+        const size_t smem = sizeof(double) * static_cast<size_t>(k) * 33;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        gather_rows_kernel<<<static_cast<unsigned>((rows + 31) / 32), k >= 256 ? 256 : 128, smem, stream>>>(
+            A, lda, rows, cols, k, C);
+        return cudaGetLastError();
+    }
     gather_columns_kernel<<<static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8)), 256, 0, stream>>>(
         A, lda, rows, cols, k, rows_of_a, C);
     return cudaGetLastError();
