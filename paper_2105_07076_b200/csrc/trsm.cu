@@ -12,6 +12,7 @@
 // checked while R11 is gathered; the host maps it to SingularMatrixError
 // (sketch) or NotPositiveDefiniteError (deterministic, solve.cpp:66-68).
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -83,6 +84,142 @@ id_trsm_kernel(const double* __restrict__ W, int64_t ldw, const double* __restri
         const long long p = pos[col];
         Z[col * k + i] = p < k ? (i == p ? 1.0 : 0.0) : X[c * ldx + i];
     }
+}
+
+// Blocked back substitution on the DMMA pipe (solve.cpp:43-51 restated for
+// many right-hand sides): a CTA takes kDmmaNB columns of W's top k rows into
+// shared memory with R11 (k padded to 32*NBLK with an identity block), then
+// bottom-up per 32-row block b:
+//   X_b   <- R_bb^-1 X_b       substitution, one thread per right-hand side
+//                              (reciprocal diagonal, R_bb read by broadcast)
+//   X_top <- X_top - R_{top,b} X_b   m8n8k4 DMMA tiles over the rows above
+// The update carries the (k^2/2)(n) flops of the solve on the tensor pipe; the
+// diagonal solves are 32 dependent steps per block.
+constexpr int kDmmaNB = 64;       // right-hand sides per CTA
+constexpr int kDmmaThreads = 128;
+
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int NBLK>
+__global__ void __launch_bounds__(kDmmaThreads)
+id_trsm_dmma_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ R11, int k, int64_t n,
+                    const long long* __restrict__ pos, double* __restrict__ Z) {
+    constexpr int KP = 32 * NBLK;
+    constexpr int LD = KP + 4;  // = 4 (mod 16) doubles: fragment loads are bank-conflict free
+    extern __shared__ __align__(16) double smem[];
+    double* Rs = smem;                    // KP x KP, column-major, stride LD
+    double* Xs = Rs + KP * LD;            // kDmmaNB right-hand sides, stride LD
+    double* rinv = Xs + kDmmaNB * LD;     // KP
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kDmmaNB;
+    const int nb = static_cast<int>(min(static_cast<long long>(kDmmaNB), static_cast<long long>(n - c0)));
+
+    // operands land by cp.async (all loads in flight at once); padding is written directly
+    for (int e = tid; e < KP * KP; e += kDmmaThreads) {
+        const int col = e / KP, row = e - col * KP;
+        double* dst = Rs + col * LD + row;
+        if (row < k && col < k) cp_async_8(dst, R11 + static_cast<int64_t>(col) * k + row);
+        else *dst = row == col ? 1.0 : 0.0;
+    }
+    for (int e = tid; e < kDmmaNB * KP; e += kDmmaThreads) {
+        const int c = e / KP, row = e - c * KP;
+        double* dst = Xs + c * LD + row;
+        if (c < nb && row < k) cp_async_8(dst, W + (c0 + c) * ldw + row);
+        else *dst = 0.0;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    for (int row = tid; row < KP; row += kDmmaThreads) rinv[row] = 1.0 / Rs[row * LD + row];
+    __syncthreads();
+
+#pragma unroll 1
+    for (int b = NBLK - 1; b >= 0; --b) {
+        const int r0 = 32 * b;
+        if (tid < kDmmaNB) {  // X_b <- R_bb^-1 X_b for right-hand side tid
+            double x[32];
+            double* xc = Xs + tid * LD + r0;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) x[r] = xc[r];
+            const double* rb = Rs + r0 * LD + r0;
+#pragma unroll
+            for (int i = 31; i >= 0; --i) {
+                x[i] *= rinv[r0 + i];
+#pragma unroll
+                for (int l = 0; l < i; ++l) x[l] = fma(-rb[i * LD + l], x[i], x[l]);
+            }
+#pragma unroll
+            for (int r = 0; r < 32; ++r) xc[r] = x[r];
+        }
+        __syncthreads();
+        // rows [0, r0): a warp takes one 8-row tile across all 8 column tiles
+        // (8 independent accumulators share each A fragment), k-depth 32
+        for (int rt = warp; rt < 4 * b; rt += kDmmaThreads / 32) {
+            const int row = rt * 8 + fr;
+            double acc[kDmmaNB / 8][2];
+#pragma unroll
+            for (int ct = 0; ct < kDmmaNB / 8; ++ct) {
+                acc[ct][0] = Xs[(ct * 8 + 2 * fc) * LD + row];
+                acc[ct][1] = Xs[(ct * 8 + 2 * fc + 1) * LD + row];
+            }
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int kk = r0 + ks * 4 + fc;
+                const double a = -Rs[kk * LD + row];
+#pragma unroll
+                for (int ct = 0; ct < kDmmaNB / 8; ++ct) dmma_8x8x4(acc[ct], a, Xs[(ct * 8 + fr) * LD + kk]);
+            }
+#pragma unroll
+            for (int ct = 0; ct < kDmmaNB / 8; ++ct) {
+                Xs[(ct * 8 + 2 * fc) * LD + row] = acc[ct][0];
+                Xs[(ct * 8 + 2 * fc + 1) * LD + row] = acc[ct][1];
+            }
+        }
+        __syncthreads();
+    }
+
+    // Z columns: the warp's positions are loaded up front (one round trip), then
+    // coalesced stores along each column
+    constexpr int kPer = kDmmaNB / (kDmmaThreads / 32);  // columns per warp (16)
+    const long long mp = (lane < kPer && warp + (kDmmaThreads / 32) * lane < nb)
+                             ? pos[c0 + warp + (kDmmaThreads / 32) * lane] : 0;
+#pragma unroll 4
+    for (int t = 0; t < kPer; ++t) {
+        const int c = warp + (kDmmaThreads / 32) * t;
+        const long long p = __shfl_sync(0xffffffffu, mp, t);
+        if (c < nb) {
+            const int64_t col = c0 + c;
+            for (int i = lane; i < k; i += 32) Z[col * k + i] = p < k ? (i == p ? 1.0 : 0.0) : Xs[c * LD + i];
+        }
+    }
+}
+
+template <int NBLK>
+size_t trsm_dmma_smem() {
+    constexpr int KP = 32 * NBLK, LD = KP + 4;
+    return sizeof(double) * (static_cast<size_t>(KP) * LD + static_cast<size_t>(kDmmaNB) * LD + KP);
+}
+
+template <int NBLK>
+cudaError_t launch_trsm_dmma(const double* W, int64_t ldw, const double* R11, int k, int64_t n,
+                             const long long* pos, double* Z, cudaStream_t stream) {
+    const size_t smem = trsm_dmma_smem<NBLK>();
+    cudaError_t e = cudaFuncSetAttribute(id_trsm_dmma_kernel<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (n + kDmmaNB - 1) / kDmmaNB;
+    id_trsm_dmma_kernel<NBLK><<<static_cast<unsigned>(blocks), kDmmaThreads, smem, stream>>>(W, ldw, R11, k, n, pos, Z);
+    return cudaGetLastError();
 }
 
 // Warp-independent back substitution (solve.cpp:43-51 restated): each warp
@@ -328,6 +465,15 @@ cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int
     W += c_begin * ldw;
     pos += c_begin;
     if (n <= 0) return cudaGetLastError();
+    const char* te = getenv("IDK_TRSM_DMMA");
+    if (k <= 128 && !(te && atoi(te) == 0)) {
+        switch ((k + 31) / 32) {
+            case 1: return launch_trsm_dmma<1>(W, ldw, R11, k, n, pos, Z, stream);
+            case 2: return launch_trsm_dmma<2>(W, ldw, R11, k, n, pos, Z, stream);
+            case 3: return launch_trsm_dmma<3>(W, ldw, R11, k, n, pos, Z, stream);
+            default: return launch_trsm_dmma<4>(W, ldw, R11, k, n, pos, Z, stream);
+        }
+    }
     switch ((k + 31) / 32) {
         case 1: return launch_trsm_warp<1>(W, ldw, R11, k, n, pos, Z, stream);
         case 2: return launch_trsm_warp<2>(W, ldw, R11, k, n, pos, Z, stream);
