@@ -75,7 +75,7 @@ def launches():
         a[1] += v
     tot = sum(v[1] for v in agg.values())
     lines = ["ncu launch list (gpu__time_duration.sum, --clock-control none, serialised by ncu) of "
-             "`python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e` (cfg2, 8 IDs per step), "
+             "`python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e` (cfg2, 48 IDs per step), "
              "our kernels only (-k filter in tools/gpu_profiles.sh):",
              f"{'kernel':58s} {'launches':>8s} {'total us':>10s} {'avg us':>9s} {'share':>6s}"]
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -113,12 +113,16 @@ def full():
             if st and "dram_bytes" in it:
                 per.setdefault(st, []).append(it["dram_bytes"])
         summary[c] = {st: {"dram_bytes_per_launch": sum(v) / len(v)} for st, v in per.items()}
+        def nv(it, key):
+            v = it.get(key, 0)
+            return v if isinstance(v, float) else 0.0
+
         for it in res:
-            table.append(f"{c:5s} {it['kernel'][:44]:44s} {it.get('duration_ns', 0) / 1e3:9.1f} us  "
-                         f"dram {it.get('dram_bytes', 0) / 1e6:9.2f} MB ({it.get('dram_pct_of_peak', 0):5.1f}% peak)  "
-                         f"sm {it.get('sm_throughput_pct', 0):5.1f}%  fp64pipe {it.get('fp64_pipe_cycles_pct', 0):5.1f}%  "
-                         f"tensor(DMMA) {it.get('tensor_pipe_pct', 0):5.1f}%  "
-                         f"shared {it.get('shared_pipe_pct', 0):5.1f}%  occ {it.get('achieved_occupancy_pct', 0):5.1f}%")
+            table.append(f"{c:5s} {it['kernel'][:44]:44s} {nv(it, 'duration_ns') / 1e3:9.1f} us  "
+                         f"dram {nv(it, 'dram_bytes') / 1e6:9.2f} MB ({nv(it, 'dram_pct_of_peak'):5.1f}% peak)  "
+                         f"sm {nv(it, 'sm_throughput_pct'):5.1f}%  fp64pipe {nv(it, 'fp64_pipe_cycles_pct'):5.1f}%  "
+                         f"tensor(DMMA) {nv(it, 'tensor_pipe_pct'):5.1f}%  "
+                         f"shared {nv(it, 'shared_pipe_pct'):5.1f}%  occ {nv(it, 'achieved_occupancy_pct'):5.1f}%")
     summary["source"] = f"profiles/ncu_full_{tag}.json (ncu --set full --clock-control none, tools/gpu_profiles.sh)"
     json.dump(allres, open(os.path.join(PROF, f"ncu_full_{tag}.json"), "w"), indent=1)
     json.dump(summary, open(os.path.join(PROF, f"ncu_summary_{tag}.json"), "w"), indent=1)
