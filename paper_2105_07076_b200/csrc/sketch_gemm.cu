@@ -22,8 +22,14 @@ namespace idk {
 namespace {
 
 constexpr int kBN = 64;
-constexpr int kBK = 16;
-constexpr int kStages = 2;
+#ifndef IDK_GEMM_BK
+#define IDK_GEMM_BK 16
+#endif
+#ifndef IDK_GEMM_STAGES
+#define IDK_GEMM_STAGES 2
+#endif
+constexpr int kBK = IDK_GEMM_BK;
+constexpr int kStages = IDK_GEMM_STAGES;
 constexpr int kThreads = 128;
 
 __device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, bool pred) {

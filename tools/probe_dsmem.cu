@@ -14,6 +14,8 @@
 //   9 15 warps issue one bulk push each
 //  10 warp 0: st.async 16-B remote stores of hdr+rows to every peer (mbarrier tx)
 //  11 warps 0..14: warp w st.async's hdr+rows to peer w (mbarrier tx)
+//  12 warp 0: hdr+rows stored to a global slot, then ONE cp.async.bulk
+//     global -> shared::cluster .multicast::cluster to all 16 CTAs (mbarrier tx)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/probe_dsmem tools/probe_dsmem.cu
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -54,6 +56,13 @@ __device__ __forceinline__ void st_async_v2(unsigned a, double x, double y, unsi
                  "d"(y), "r"(mbar)
                  : "memory");
 }
+__device__ __forceinline__ void bulk_mcast(unsigned dst, const void* src, unsigned bytes, unsigned mbar,
+                                           unsigned short mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mbar), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cl(unsigned a, unsigned par) {
     asm volatile(
         "{\n\t.reg .pred p;\nWC_%=:\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t@!p bra WC_%=;\n}" ::"r"(a),
@@ -70,7 +79,7 @@ __device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) {
 constexpr int G = 16;
 constexpr int HDR = 6;
 
-__global__ void __cluster_dims__(G, 1, 1) probe(int variant, int rows, int rounds, long long* out) {
+__global__ void __cluster_dims__(G, 1, 1) probe(int variant, int rows, int rounds, long long* out, double* gslots) {
     extern __shared__ __align__(16) double sm[];
     __shared__ unsigned long long mbar[2];
     __shared__ unsigned long long mbar2[2];
@@ -196,6 +205,19 @@ __global__ void __cluster_dims__(G, 1, 1) probe(int variant, int rows, int round
             }
             mbar_wait(mb, (phase >> p) & 1u);
             phase ^= 1u << p;
+        } else if (variant == 12) {
+            const unsigned mb = smem_u32(&mbar[p]);
+            const int per = HDR + rows;
+            if (tid == 0) mbar_expect_tx(mb, G * per * 8);
+            if (threadIdx.x < 32) {
+                double* gs = gslots + (static_cast<size_t>(p) * G + me) * slot;
+                for (int i = threadIdx.x; i < per; i += 32) gs[i] = own[i];
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __syncwarp();
+                if (threadIdx.x == 0) bulk_mcast(smem_u32(own), gs, per * 8, mb, 0xffff);
+            }
+            mbar_wait(mb, (phase >> p) & 1u);
+            phase ^= 1u << p;
         } else if (variant == 3) {
             if (tid < G && tid != me) {
                 double* dst = cl.map_shared_rank(own, tid);
@@ -226,18 +248,20 @@ __global__ void __cluster_dims__(G, 1, 1) probe(int variant, int rows, int round
 int main() {
     long long* out;
     cudaMalloc(&out, 16);
+    double* gslots;
+    cudaMalloc(&gslots, sizeof(double) * 2 * G * (HDR + 512));
     const char* names[] = {"cluster.sync only", "bulk push hdr+rows (2/peer) + mbar", "bulk push 1/peer + mbar",
                            "st.cluster hdr + cluster.sync + ld.cluster rows", "st.cluster hdr+rows + cluster.sync",
                            "bulk push hdr + mbar + ld.cluster rows", "warp0 st.cluster hdr + remote arrive",
                            "warp0 st.cluster hdr + remote arrive + ld.cluster rows", "warp0 bulk push 1/peer + mbar",
-                           "15 warps x 1 bulk push + mbar", "warp0 st.async hdr+rows to all peers", "warp w st.async hdr+rows to peer w"};
+                           "15 warps x 1 bulk push + mbar", "warp0 st.async hdr+rows to all peers", "warp w st.async hdr+rows to peer w", "warp0 global slot + 1 multicast bulk copy"};
     for (int rows : {112, 272, 512}) {
-        for (int v = 0; v < 12; ++v) {
+        for (int v = 0; v < 13; ++v) {
             const size_t smem = sizeof(double) * 2 * G * (HDR + rows);
             cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaMemset(out, 0, 16);
-            probe<<<G, 512, smem>>>(v, rows, 2000, out);
+            probe<<<G, 512, smem>>>(v, rows, 2000, out, gslots);
             cudaError_t e = cudaGetLastError();
             long long h = -1;
             if (e == cudaSuccess) e = cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
