@@ -204,6 +204,118 @@ id_trsm_dmma_kernel(const double* __restrict__ W, int64_t ldw, const double* __r
     }
 }
 
+// k in (128, 256]: R11 (up to 512 KB) stays in global memory (L2-resident):
+// the DMMA A fragments are read from it directly (all 8 k-steps of a row
+// tile issued before the first DMMA) and each 32x32 diagonal block is staged
+// in shared memory for its substitution.  X (64 right-hand sides) and the
+// reciprocal diagonal live in shared memory.
+template <int NBLK>
+__global__ void __launch_bounds__(kDmmaThreads)
+id_trsm_dmma_big_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ R11, int k, int64_t n,
+                        const long long* __restrict__ pos, double* __restrict__ Z) {
+    constexpr int KP = 32 * NBLK;
+    constexpr int LD = KP + 4;
+    constexpr int LDB = 32 + 1;  // diagonal block, column-major
+    extern __shared__ __align__(16) double smem[];
+    double* Xs = smem;                     // kDmmaNB right-hand sides, stride LD
+    double* Db = Xs + kDmmaNB * LD;        // 32 x 32 diagonal block
+    double* rinv = Db + 32 * LDB;          // KP
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kDmmaNB;
+    const int nb = static_cast<int>(min(static_cast<long long>(kDmmaNB), static_cast<long long>(n - c0)));
+    // R[row, col] with the identity padding beyond k
+    auto rget = [&](int row, int col) -> double {
+        return (row < k && col < k) ? __ldg(R11 + static_cast<int64_t>(col) * k + row) : (row == col ? 1.0 : 0.0);
+    };
+
+    for (int e = tid; e < kDmmaNB * KP; e += kDmmaThreads) {
+        const int c = e / KP, row = e - c * KP;
+        double* dst = Xs + c * LD + row;
+        if (c < nb && row < k) cp_async_8(dst, W + (c0 + c) * ldw + row);
+        else *dst = 0.0;
+    }
+    for (int row = tid; row < KP; row += kDmmaThreads) rinv[row] = 1.0 / rget(row, row);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+
+#pragma unroll 1
+    for (int b = NBLK - 1; b >= 0; --b) {
+        const int r0 = 32 * b;
+        for (int e = tid; e < 32 * 32; e += kDmmaThreads) {
+            const int col = e >> 5, row = e & 31;
+            Db[col * LDB + row] = rget(r0 + row, r0 + col);
+        }
+        __syncthreads();
+        if (tid < kDmmaNB) {
+            double x[32];
+            double* xc = Xs + tid * LD + r0;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) x[r] = xc[r];
+#pragma unroll
+            for (int i = 31; i >= 0; --i) {
+                x[i] *= rinv[r0 + i];
+#pragma unroll
+                for (int l = 0; l < i; ++l) x[l] = fma(-Db[i * LDB + l], x[i], x[l]);
+            }
+#pragma unroll
+            for (int r = 0; r < 32; ++r) xc[r] = x[r];
+        }
+        __syncthreads();
+        for (int rt = warp; rt < 4 * b; rt += kDmmaThreads / 32) {
+            const int row = rt * 8 + fr;
+            double af[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) af[ks] = -rget(row, r0 + ks * 4 + fc);
+            double acc[kDmmaNB / 8][2];
+#pragma unroll
+            for (int ct = 0; ct < kDmmaNB / 8; ++ct) {
+                acc[ct][0] = Xs[(ct * 8 + 2 * fc) * LD + row];
+                acc[ct][1] = Xs[(ct * 8 + 2 * fc + 1) * LD + row];
+            }
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int kk = r0 + ks * 4 + fc;
+#pragma unroll
+                for (int ct = 0; ct < kDmmaNB / 8; ++ct) dmma_8x8x4(acc[ct], af[ks], Xs[(ct * 8 + fr) * LD + kk]);
+            }
+#pragma unroll
+            for (int ct = 0; ct < kDmmaNB / 8; ++ct) {
+                Xs[(ct * 8 + 2 * fc) * LD + row] = acc[ct][0];
+                Xs[(ct * 8 + 2 * fc + 1) * LD + row] = acc[ct][1];
+            }
+        }
+        __syncthreads();
+    }
+
+    constexpr int kPer = kDmmaNB / (kDmmaThreads / 32);
+    const long long mp = (lane < kPer && warp + (kDmmaThreads / 32) * lane < nb)
+                             ? pos[c0 + warp + (kDmmaThreads / 32) * lane] : 0;
+#pragma unroll 4
+    for (int t = 0; t < kPer; ++t) {
+        const int c = warp + (kDmmaThreads / 32) * t;
+        const long long p = __shfl_sync(0xffffffffu, mp, t);
+        if (c < nb) {
+            const int64_t col = c0 + c;
+            for (int i = lane; i < k; i += 32) Z[col * k + i] = p < k ? (i == p ? 1.0 : 0.0) : Xs[c * LD + i];
+        }
+    }
+}
+
+template <int NBLK>
+cudaError_t launch_trsm_dmma_big(const double* W, int64_t ldw, const double* R11, int k, int64_t n,
+                                 const long long* pos, double* Z, cudaStream_t stream) {
+    constexpr int KP = 32 * NBLK, LD = KP + 4;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(kDmmaNB) * LD + 32 * 33 + KP);
+    cudaError_t e = cudaFuncSetAttribute(id_trsm_dmma_big_kernel<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (n + kDmmaNB - 1) / kDmmaNB;
+    id_trsm_dmma_big_kernel<NBLK><<<static_cast<unsigned>(blocks), kDmmaThreads, smem, stream>>>(W, ldw, R11, k, n,
+                                                                                                   pos, Z);
+    return cudaGetLastError();
+}
+
 template <int NBLK>
 size_t trsm_dmma_smem() {
     constexpr int KP = 32 * NBLK, LD = KP + 4;
@@ -472,6 +584,14 @@ cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int
             case 2: return launch_trsm_dmma<2>(W, ldw, R11, k, n, pos, Z, stream);
             case 3: return launch_trsm_dmma<3>(W, ldw, R11, k, n, pos, Z, stream);
             default: return launch_trsm_dmma<4>(W, ldw, R11, k, n, pos, Z, stream);
+        }
+    }
+    if (k <= 256 && !(te && atoi(te) == 0)) {
+        switch ((k + 31) / 32) {
+            case 5: return launch_trsm_dmma_big<5>(W, ldw, R11, k, n, pos, Z, stream);
+            case 6: return launch_trsm_dmma_big<6>(W, ldw, R11, k, n, pos, Z, stream);
+            case 7: return launch_trsm_dmma_big<7>(W, ldw, R11, k, n, pos, Z, stream);
+            default: return launch_trsm_dmma_big<8>(W, ldw, R11, k, n, pos, Z, stream);
         }
     }
     switch ((k + 31) / 32) {

@@ -119,3 +119,38 @@ def test_zero_matrix_qr_pivots_in_order(idk, ref):
     f = idk.qr_column_pivoted(dev(a), 6)
     _, _, rperm = ref.qr_column_pivoted(a, 6)
     assert np.array_equal(host(f.perm), rperm)
+
+
+@pytest.mark.parametrize("k", [1, 2, 31, 32, 33, 63, 64, 65, 96, 100, 127, 128, 129, 160, 224, 256, 257])
+def test_z_solve_block_boundaries(idk, ref, monkeypatch, k):
+    """The DMMA blocked Z solve (k <= 128: identity-padded 32-row blocks, 64
+    right-hand sides per CTA) at every block and CTA boundary, against the
+    reference and against the warp kernel it replaces (IDK_TRSM_DMMA=0)."""
+    m, n = k + 7, 2 * k + 71  # n - k right-hand sides: not a multiple of 64
+    a = ref.gaussian_matrix(m, n, 40 + k)
+    a[:, ::5] *= 3.0
+    rcols, rz, _, _ = ref.id_auto(a, k, False)
+    r = idk.id_auto(dev(a), k, idk.DETERMINISTIC)
+    assert np.array_equal(host(r.cols), rcols)
+    assert rel(host(r.z), rz) <= ZTOL
+    monkeypatch.setenv("IDK_TRSM_DMMA", "0")
+    w = idk.id_auto(dev(a), k, idk.DETERMINISTIC)
+    assert np.array_equal(host(w.cols), host(r.cols))
+    assert rel(host(w.z), host(r.z)) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,k,padded_ld", [(37, 50, 5, False), (64, 300, 17, True), (2000, 300, 120, False),
+                                            (301, 77, 9, True), (2000, 40, 800, False)])
+def test_select_columns_all_paths(idk, ref, m, n, k, padded_ld):
+    """select_columns (matrix.cpp:121-130) through the vectorised column copy
+    (even rows, 16-byte aligned), its scalar fallback (odd rows / padded ld) and
+    the staged row gather of the dual: bit-exact."""
+    import torch
+    a = ref.gaussian_matrix(m, n, 5 + m)
+    da = padded(a, extra=3) if padded_ld else dev(a)
+    cols = np.random.default_rng(m + n).choice(n, size=min(k, n), replace=False)
+    c = host(idk.select_columns(da, torch.from_numpy(cols).cuda()))
+    assert np.array_equal(c, a[:, cols])
+    rows = np.random.default_rng(m).choice(m, size=min(k, m), replace=False)
+    cr = host(idk.select_columns(da, torch.from_numpy(rows).cuda(), rows_of_a=True))
+    assert np.array_equal(cr, a[rows, :].T)

@@ -1,4 +1,4 @@
-python -m pytest tests -x -q -m gpu -k "id or rid or config or edge" > gpurun_out/t_all.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/t_all.log
-for T in 1 0; do for c in cfg2; do IDK_TRSM_DMMA=$T python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('dmma=$T $c', round(d['value'],1), d['ms_per_step'], {k: round(v,4) for k,v in d['stages_ms_per_step'].items()})"; done; done
-python tools/prof_id.py cfg2 2 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:trsm -c 1 python tools/prof_id.py cfg2 2 2>&1 | grep -E "trsm|duration" | head -8
-python tools/prof_id.py cfg2 2 > /dev/null 2>&1 && ncu --set full --import-source on --clock-control none -k regex:trsm -c 1 -o gpurun_out/trsm2 -f python tools/prof_id.py cfg2 2 > /dev/null 2>&1; ncu -i gpurun_out/trsm2.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/src_trsm2.csv 2>/dev/null; rm -f gpurun_out/trsm2.ncu-rep
+python -m pytest tests/test_gpu_edges.py -x -q > gpurun_out/t_edges.log 2>&1; echo edges rc=$?; tail -3 gpurun_out/t_edges.log
+python -m pytest tests -x -q -m gpu > gpurun_out/t_all.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/t_all.log
+for T in 1 0; do IDK_TRSM_DMMA=$T python bench.py --config cfg4 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('dmma=$T cfg4', round(d['value'],1), d['ms_per_step'], {k: round(v,4) for k,v in d['stages_ms_per_step'].items()})"; done
+python tools/prof_id.py cfg4 1 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:trsm -c 1 python tools/prof_id.py cfg4 1 2>&1 | grep -E "trsm|duration" | head -4
