@@ -180,9 +180,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # IDK_BENCH_BACKEND=gloo + more ranks than GPUs: plumbing check of the N > 1
+    # path on a one-GPU box (ranks share a device; not a measurement)
+    backend = os.environ.get("IDK_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cfg = CONFIGS[args.config]
     dev = torch.device("cuda", local)
     k, p = cfg.k, max(cfg.p, 0)
