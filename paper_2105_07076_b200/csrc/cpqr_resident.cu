@@ -246,7 +246,7 @@ cpqr_resident_kernel(ResidentArgs a) {
     // cluster slots, 16-B aligned: push mode [3][G][cslot]; pull mode [3][cslot]
     // (own) followed by the header copies [3][G][kCHdr]
     double* cslots = reinterpret_cast<double*>(s_pos + nc);
-    cslots += (reinterpret_cast<uintptr_t>(cslots) >> 3) & 1;
+    cslots += (static_cast<unsigned>(__cvta_generic_to_shared(cslots)) >> 3) & 1u;  // 16-B align (stays a shared-window pointer)
     const bool push = a.push != 0;
     double* chdr = cslots + 3 * cslot;
 
