@@ -162,6 +162,7 @@ __device__ __forceinline__ void reflector_warp(double alpha, double tail, int le
 }
 
 constexpr int kPubRegs = 4;  // candidate rows per lane kept in registers (m - first <= 128)
+constexpr int kHelpWarps = 4;  // warps building a tall (m - first > 128) candidate
 
 __device__ __forceinline__ unsigned long long tagged(unsigned payload, unsigned tag) {
     return (static_cast<unsigned long long>(payload) << 32) | tag;
@@ -255,6 +256,7 @@ cpqr_resident_kernel(ResidentArgs a) {
     __shared__ unsigned s_wp[32];
     __shared__ unsigned s_wl[32];
     __shared__ long long s_sel[3];  // grid tie pass: -, winning position, winning CTA
+    __shared__ double s_help[kHelpWarps + 2];  // tall candidate build: partial norms, pending w, alpha
     __shared__ unsigned long long s_mbar[2];      // cluster: bulk-push barriers, one per slot parity
     __shared__ double s_rv[kCluster ? 1 : 160];  // grid: the G records of this exchange
     __shared__ unsigned s_rp[kCluster ? 1 : 160];
@@ -512,8 +514,124 @@ cpqr_resident_kernel(ResidentArgs a) {
         // The warp holding the winner column builds the next reflector with all
         // 32 lanes (its deferred update applied on the fly to a raw copy), so
         // the serial path is a few rows per lane, not the group's whole column.
-        const bool pubwarp = wid == (have ? (winlc * S) >> 5 : 0);
-        if (pubwarp) {
+        const int pw = have ? (winlc * S) >> 5 : 0;
+        const bool pubwarp = wid == pw;
+        // Tall candidates (pull mode, m - first > 32 * kPubRegs) are built by
+        // kHelpWarps warps (the publishing warp and the ones after it): each
+        // takes every kHelpWarps-th 32-row slice, the partial norms meet in
+        // shared memory (named barrier 2), every helper evaluates the same
+        // reflector and scales its own rows.
+        // (compiled for S >= 4 only: the S = 1, 2 kernels serve m <= 128 in practice and
+        // keep their register budget for the resident rows)
+        const bool tall = S >= 4 && have && (m - first > 32 * kPubRegs);
+        const int nh = tall ? min(kHelpWarps, nw) : 1;
+        const int hi = (wid - pw + nw) % nw;
+        bool built = false;
+        if constexpr (S >= 4) {
+        if (tall && hi < nh) {
+            built = true;
+            double* own = own_slot(sl);
+            double* hd = own + xlen;
+            const int lo = max(0, first - 2) & ~1;
+            const unsigned bytes = push ? static_cast<unsigned>(xlen + kCHdr - lo) * sizeof(double)
+                                        : static_cast<unsigned>(kCHdr * sizeof(double));
+            const unsigned nthr = static_cast<unsigned>(nh * 32);
+            if (pubwarp) {
+                const int wl0 = (winlc * S) & 31;
+                const double w0 = __shfl_sync(kFull, todo ? wpend : 0.0, wl0);  // 0: already current
+                if (lc == winlc) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int i = l0 + q + S * r;
+                        if (i >= first && i < m) xbuf[i] = yr[r];
+                    }
+                }
+                if (lane == 0) s_help[kHelpWarps] = w0;
+            }
+            asm volatile("bar.sync 2, %0;" ::"r"(nthr) : "memory");
+            trace_by(pubwarp && lane == 0, step, 8);
+            const double ww = s_help[kHelpWarps];
+            const double* wrow = rows + static_cast<size_t>(winlc) * lds;
+            const int stride = 32 * nh;
+            double tl = 0.0;
+            for (int i0 = first + 32 * hi + lane; i0 < m; i0 += stride * kPubRegs) {
+                double yv[kPubRegs];
+#pragma unroll
+                for (int t = 0; t < kPubRegs; ++t) {
+                    const int i = i0 + stride * t;
+                    yv[t] = i < m ? fma(-ww, xa[i], i < l0 ? wrow[i] : xbuf[i]) : 0.0;  // the group's axpy
+                }
+#pragma unroll
+                for (int t = 0; t < kPubRegs; ++t) {
+                    const int i = i0 + stride * t;
+                    if (i < m) {
+                        xbuf[i] = yv[t];
+                        if (i == first) s_help[kHelpWarps + 1] = yv[t];
+                        else tl = fma(yv[t], yv[t], tl);
+                    }
+                }
+            }
+            tl = warp_sum(tl);
+            if (lane == 0) s_help[hi] = tl;
+            asm volatile("bar.sync 2, %0;" ::"r"(nthr) : "memory");
+            double tt = 0.0;
+            for (int h = 0; h < nh; ++h) tt += s_help[h];  // fixed order: every helper gets the same sum
+            const double al = s_help[kHelpWarps + 1];
+            trace_by(pubwarp && lane == 0, step, 9);
+            double tu, be, sc;
+            reflector_warp(al, tt, m - first, tu, be, sc);
+            trace_by(pubwarp && lane == 0, step, 10);
+            for (int i0 = first + 32 * hi + lane; i0 < m; i0 += stride * kPubRegs) {
+                double yv[kPubRegs];
+#pragma unroll
+                for (int t = 0; t < kPubRegs; ++t) yv[t] = i0 + stride * t < m ? xbuf[i0 + stride * t] : 0.0;
+#pragma unroll
+                for (int t = 0; t < kPubRegs; ++t) {
+                    const int i = i0 + stride * t;
+                    if (i < m) own[i] = tu != 0.0 ? (i == first ? 1.0 : mul_rn(yv[t], sc)) : yv[t];
+                }
+            }
+            asm volatile("bar.sync 2, %0;" ::"r"(nthr) : "memory");  // every row of v is in the slot
+            if (pubwarp) {
+                if (lane == 0) {
+                    hd[0] = __longlong_as_double(c0 + winlc);
+                    hd[1] = tu;
+                    hd[2] = be;
+                    hd[3] = sc;
+                }
+                if (lane < first - lo) own[lo + lane] = 0.0;  // retired rows read v = 0
+                if (lane == 0) {
+                    hd[4] = have ? mx : -1.0;
+                    hd[5] = __longlong_as_double(have ? static_cast<long long>(winpos) : 0xffffffffLL);
+                    if (!push) {
+                        double* mine = hdr_of(sl, me);
+                        for (int j = 0; j < kCHdr; ++j) mine[j] = hd[j];
+                    }
+                }
+                trace_by(lane == 0, step, 11);
+                fence_proxy_async_smem();  // staging writes (generic proxy) -> bulk-copy reads (async proxy)
+                __syncwarp();
+                trace_by(lane == 0, step, 12);
+                // the arrive releases the local staging to this CTA's waiters; the
+                // peers' copies complete the transaction count
+                if (lane == 0) mbar_expect_tx(mb, static_cast<unsigned>(G - 1) * bytes);
+                if (lane < G - 1) {
+                    const int g = lane < me ? lane : lane + 1;
+                    const unsigned sa = smem_u32(push ? own + lo : hd);
+                    const unsigned da = push ? sa : smem_u32(hdr_of(sl, me));
+                    bulk_push(mapa_u32(da, g), sa, bytes, mapa_u32(mb, g));
+                }
+                trace_by(lane == 0, step, 3);
+                // let the other warps go: their axpys contend for shared memory, so
+                // they wait until the candidate is out (named barrier 1)
+                asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
+            } else {
+                asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
+            }
+        }
+        }
+        if (built) {
+        } else if (pubwarp) {
             double* own = own_slot(sl);
             double* hd = own + xlen;
             const int lo = max(0, first - 2) & ~1;
