@@ -113,10 +113,16 @@ __device__ __forceinline__ long long globaltimer() {
 
 // sqrt(v) >= (1 - 1e-14) * sqrt(vmax) (qr.cpp:71-73) evaluated exactly, with
 // the sqrt only inside the 4e-14 band where the answer is not obvious.
+// The sqrt pair is out of line: the band test almost never reaches it, and
+// inlined at every reduction site it was ~750 SASS instructions of cold code
+// inside the step loop (instruction-fetch stalls on the serial phases).
+__device__ __noinline__ bool qualifies_band(double v, double vmax) {
+    return sqrt(v) >= (1.0 - 1e-14) * sqrt(vmax);
+}
 __device__ __forceinline__ bool qualifies(double v, double vmax) {
     if (v == vmax) return true;
     if (!(v >= vmax * (1.0 - 4e-14))) return false;
-    return sqrt(v) >= (1.0 - 1e-14) * sqrt(vmax);
+    return qualifies_band(v, vmax);
 }
 
 // Warp max of non-negative doubles (or -1 = none) via two 32-bit redux.sync.
@@ -876,6 +882,7 @@ cpqr_resident_kernel(ResidentArgs a) {
 #pragma unroll
             for (int t = 0; t < kRecPerLane; ++t) vmax = fmax(vmax, v[t]);
             vmax = warp_max_nonneg(vmax);
+            trace(step, 13);
             unsigned best = 0xffffffffu;
             int bt = 0, amb = 0;
 #pragma unroll
@@ -893,6 +900,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             // positions are distinct, so exactly one lane holds the minimum
             gsel = static_cast<int>(__reduce_min_sync(
                 kFull, (best == wsel && best != 0xffffffffu) ? static_cast<unsigned>(lane + 32 * bt) : 0xffffffffu));
+            trace(step, 14);
             if (amb) {
                 // Exact tie pass: lowest position with sqrt(live) >= the global threshold.
                 int winlc;

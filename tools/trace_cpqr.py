@@ -61,6 +61,10 @@ if t[:, :steps, 8].max() > 0:  # cluster publish path of the winner warp (marks 
     for nm, a0, a1 in pw:
         d = t[:, :steps, a1] - t[:, :steps, a0]
         print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+if t[:, :steps, 13].max() > 0:  # grid select: records -> vmax -> winner (before the tie pass) -> done
+    for nm, a0, a1 in [("  records -> vmax", 4, 13), ("  vmax -> winner", 13, 14), ("  tie pass / rest", 14, 5)]:
+        d = t[:, :steps, a1] - t[:, :steps, a0]
+        print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
 for lo, hi in [(0, 10), (k // 2 - 5, k // 2 + 5), (steps - 10, steps)]:
     dd = [(t[:, lo:hi, i + 1] - t[:, lo:hi, i]).mean() for i in range(6)]
     print(f"  steps {lo:3d}-{hi:3d}: " + " ".join(f"{x:7.0f}" for x in dd))
