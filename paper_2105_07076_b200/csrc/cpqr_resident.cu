@@ -1127,10 +1127,30 @@ cpqr_resident_kernel(ResidentArgs a) {
             lv = sub_rn(live0, mul_rn(head, head));
             if (lv < 0.0) lv = 0.0;
             if (lv <= mul_rn(kRecomp, anchor0)) {
-                // fresh = sum_{i > s} y_i^2 (qr.cpp:101-104) of the updated column
-                do_axpy();
-                double al, tl;
-                partials(s + 1, al, tl);
+                // fresh = sum_{i > s} y_i^2 (qr.cpp:101-104) of the updated column,
+                // its rows formed on the fly exactly as the deferred axpy will
+                // (same fma, same summation order as partials()); the axpy stays
+                // pending, so no second inlined copy of it sits in the step loop
+                const double ww = todo ? wpend : 0.0;
+                const int first = s + 1;
+                double a0 = 0.0, t0 = 0.0, t1 = 0.0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int i = l0 + q + S * r;
+                    const double u = fma(-ww, xr[S * r], yr[r]);
+                    if (i == first) a0 = u;
+                    else if (i > first) {
+                        if (r & 1) t1 = fma(u, u, t1);
+                        else t0 = fma(u, u, t0);
+                    }
+                }
+                for (int r = first / S; r < nsr; ++r) {
+                    const int i = q + S * r;
+                    const double u = fma(-ww, xa[i], myrows[i]);
+                    if (i == first) a0 = u;
+                    else if (i > first) t0 = fma(u, u, t0);
+                }
+                const double al = group_sum<S>(a0), tl = group_sum<S>(t0 + t1);
                 lv = fma(al, al, tl);
                 if (q == 0) s_anchor[lc] = lv;
             }
@@ -1138,10 +1158,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             cand = q == 0;
         }
         trace(s, 1);
-        if (s + 1 == a.k) {
-            do_axpy();
-            break;
-        }
+        if (s + 1 == a.k) break;  // the last step's axpy runs after the loop
 
         // ---- next pivot: CTA candidate, exchange ----
         if constexpr (kCluster) cluster_round(s + 1, cand, lv, mypos, s);
@@ -1149,6 +1166,7 @@ cpqr_resident_kernel(ResidentArgs a) {
         trace(s, 6);
     }
 
+    do_axpy();
     // ---- write back (the only write of W) ----
     __syncthreads();
     if (active) {
