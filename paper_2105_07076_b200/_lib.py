@@ -9,7 +9,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libidkit_b200.so")
+LIB_PATH = os.environ.get("IDK_LIB_PATH") or os.path.join(PKG, "libidkit_b200.so")  # override: A/B of tuning builds
 
 # Every symbol include/idkit_b200.h declares, with its ctypes signature.
 _P = C.c_void_p
