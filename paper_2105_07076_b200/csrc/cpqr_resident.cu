@@ -287,6 +287,11 @@ cpqr_resident_kernel(ResidentArgs a) {
     };
     auto trace = [&](int s, int ph) { trace_by(tid == 0, s, ph); };
 
+    if (a.trace != nullptr && tid == 0) {  // debug: which SM this CTA runs on (slot 15 of row k)
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[(static_cast<size_t>(me) * (a.k + 1) + a.k) * 16 + 15] = smid;
+    }
     for (int i = tid; i < 3 * xlen; i += T) xbuf[i] = 0.0;
     if constexpr (kCluster) {
         const int zn = push ? 3 * G * cslot : 3 * cslot + 3 * G * kCHdr;

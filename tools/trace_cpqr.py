@@ -34,7 +34,9 @@ for it in range(3):
     else:
         idk.id_auto(a, cfg.k, idk.DETERMINISTIC)
 ctx.lib.idk_debug_cpqr_trace(ctx.h, None)
-t = buf.cpu().numpy().reshape(G, k + 1, 16).astype(np.float64)[:, :k, :]
+tt = buf.cpu().numpy().reshape(G, k + 1, 16)
+smid = tt[:, k, 15].copy()
+t = tt.astype(np.float64)[:, :k, :]
 steps = k - 1
 print(name, "mode", mode, "plan", plan)
 print(f"{'phase':24s} {'cta0 ns':>9s} {'mean ns':>9s} {'max ns':>9s}")
@@ -65,6 +67,13 @@ if t[:, :steps, 13].max() > 0:  # grid select: records -> vmax -> winner (before
     for nm, a0, a1 in [("  records -> vmax", 4, 13), ("  vmax -> winner", 13, 14), ("  tie pass / rest", 14, 5)]:
         d = t[:, :steps, a1] - t[:, :steps, a0]
         print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+# per-CTA lateness: when each CTA saw the exchange complete (mark 4) and published (mark 3),
+# relative to the earliest CTA of the same step, by SM id
+rel4 = (t[:, :steps, 4] - t[:, :steps, 4].min(axis=0)).mean(axis=1)
+rel3 = (t[:, :steps, 3] - t[:, :steps, 3].min(axis=0)).mean(axis=1)
+order = np.argsort(smid)
+print("per-CTA mean lateness (ns) of 'records read' / 'published', by SM id:")
+print("  " + " ".join(f"{int(smid[g])}:{rel4[g]:.0f}/{rel3[g]:.0f}" for g in order))
 for lo, hi in [(0, 10), (k // 2 - 5, k // 2 + 5), (steps - 10, steps)]:
     dd = [(t[:, lo:hi, i + 1] - t[:, lo:hi, i]).mean() for i in range(6)]
     print(f"  steps {lo:3d}-{hi:3d}: " + " ".join(f"{x:7.0f}" for x in dd))
