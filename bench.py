@@ -150,6 +150,29 @@ def stage_work(cfg, n_local):
     }
 
 
+def stage_rooflines(cfg, stage_avg, peaks, fp64_peak):
+    """Every stage against its own bound (sketch and Z solve: DMMA TFLOP/s; the
+    rest: HBM GB/s on algorithmic bytes).  With several IDs in flight the stage
+    times are per-launch durations under co-running kernels, so these fractions
+    are lower bounds of the kernels' own rates (DESIGN.md section 3 has the
+    stand-alone ncu numbers)."""
+    work = stage_work(cfg, cfg.n)
+    out = {}
+    for st, ms in stage_avg.items():
+        if ms <= 0 or st not in work:
+            continue
+        w = work[st]
+        if st in ("sketch", "solve") and "flops" in w:
+            tf = w["flops"] / (ms / 1e3) / 1e12
+            out[st] = {"bound": "tensor", "achieved": tf, "peak": fp64_peak["tflops"], "unit": "TFLOP/s",
+                       "frac": tf / fp64_peak["tflops"], "avg_launch_ms": ms}
+        else:
+            gb = w["bytes"] / (ms / 1e3) / 1e9
+            out[st] = {"bound": "hbm" if st != "cpqr" else "latency (k dependent steps)", "achieved": gb,
+                       "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gb / peaks["hbm_gbs"], "avg_launch_ms": ms}
+    return out
+
+
 def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic):
     secs = avg_ms / 1e3
     if stage == "sketch":
@@ -410,6 +433,7 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB memset, outside the events)",
                        "inputs": "resident in HBM"},
             "stages_ms_per_step": stage_avg or None,
+            "stage_rooflines": stage_rooflines(cfg, stage_avg, peaks, fp64) if stage_avg else None,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
         }
