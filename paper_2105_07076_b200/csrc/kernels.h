@@ -20,6 +20,9 @@ struct GroupSeeds {
 };
 cudaError_t sketch_gemm_group(const double* omega, int64_t ldb, bool b_trans, const GemmGroup& grp, int64_t ldc,
                               int M, int64_t N, int64_t K, int splits, double* partial, cudaStream_t stream);
+cudaError_t sketch_gemm_tma(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans, double* out,
+                            int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K, int splits, int wm,
+                            cudaStream_t stream);
 cudaError_t omega_philox_group(double* out, int64_t l, int64_t m, const GroupSeeds& seeds, int count,
                                cudaStream_t stream);
 int sketch_gemm_pick_wm(int M);

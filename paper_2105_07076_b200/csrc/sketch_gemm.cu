@@ -396,8 +396,20 @@ cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t l
     if (splits < 1) splits = 1;
     double* out = splits > 1 ? partial : Y;
     const int64_t split_stride = ldc * N;
-    cudaError_t e = b_trans ? launch_nt<true>(wm, A, lda, B, ldb, out, ldc, split_stride, M, N, K, splits, vec16, stream)
-                            : launch_nt<false>(wm, A, lda, B, ldb, out, ldc, split_stride, M, N, K, splits, vec16, stream);
+    cudaError_t e = cudaErrorNotSupported;
+    const char* te = getenv("IDK_GEMM_TMA");
+    // TMA-fed kernel (sketch_tma.cu) for the non-transposed operand: +4-5 % over the
+    // cp.async kernel on cfg2/cfg4 (same-box A/B); for the dual it ties (27.1 vs 27.2
+    // TFLOP/s at cfg5), so the dual stays on the cp.async kernel unless IDK_GEMM_TMA=2.
+    // IDK_GEMM_TMA=0 selects the cp.async kernel everywhere.
+    const int tma = te ? atoi(te) : 1;
+    if ((tma == 1 && !b_trans) || tma == 2)
+        e = sketch_gemm_tma(A, lda, B, ldb, b_trans, out, ldc, split_stride, M, N, K, splits, wm, stream);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        e = b_trans ? launch_nt<true>(wm, A, lda, B, ldb, out, ldc, split_stride, M, N, K, splits, vec16, stream)
+                    : launch_nt<false>(wm, A, lda, B, ldb, out, ldc, split_stride, M, N, K, splits, vec16, stream);
+    }
     if (e != cudaSuccess || splits == 1) return e;
     const int64_t total = static_cast<int64_t>(M) * N;
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
