@@ -173,11 +173,13 @@ def stage_rooflines(cfg, stage_avg, peaks, fp64_peak):
     return out
 
 
-def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic):
+def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic, dual=False):
     secs = avg_ms / 1e3
     if stage == "sketch":
         achieved = work["flops"] / secs / 1e12
-        return {"kernel": "sketch_gemm_kernel (DMMA m8n8k4)", "bound": "tensor", "achieved": achieved,
+        kern = ("sketch_gemm_kernel (cp.async-fed DMMA m8n8k4; the dual reads A transposed)" if dual
+                else "sketch_tma_kernel (TMA-fed DMMA m8n8k4)")
+        return {"kernel": kern, "bound": "tensor", "achieved": achieved,
                 "peak": fp64_peak["tflops"], "unit": "TFLOP/s", "frac": achieved / fp64_peak["tflops"],
                 "peak_source": fp64_peak["source"], "traffic": traffic, "avg_launch_ms": avg_ms,
                 "algorithmic_per_launch": work["flops"]}
@@ -389,7 +391,8 @@ def run_ours(args):
         stage_avg = {s_: v / n_stage for s_, v in stage_tot.items()}
         dom = max(stage_avg, key=stage_avg.get)
         traffic = (ncu.get(cfg.name) or {}).get(dom, {}).get("dram_bytes_per_launch")
-        roofline = roofline_for(dom, stage_work(cfg, cfg.n)[dom], stage_avg[dom], peaks, fp64, traffic)
+        roofline = roofline_for(dom, stage_work(cfg, cfg.n)[dom], stage_avg[dom], peaks, fp64, traffic,
+                                dual=cfg.m > cfg.n)
         # share of the device time per ID (with nb IDs in flight, per-launch times include co-running kernels)
         roofline["step_share"] = stage_avg[dom] / sum(stage_avg.values())
         if dom == "cpqr":  # k dependent pivot steps: latency-bound, report the per-step time

@@ -42,7 +42,7 @@ KEYS = {
 }
 SCALE = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6, "s": 1e9,
          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9}
-STAGE = [("sketch_gemm", "sketch"), ("splitk", "sketch"), ("cpqr", "cpqr"), ("trsm", "solve"),
+STAGE = [("sketch_gemm", "sketch"), ("sketch_tma", "sketch"), ("splitk", "sketch"), ("cpqr", "cpqr"), ("trsm", "solve"),
          ("gather_r11", "solve"), ("gather_columns", "gather"), ("omega", "prep"), ("batched", "batched")]
 
 
