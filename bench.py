@@ -157,7 +157,8 @@ def stage_rooflines(cfg, stage_avg, peaks, fp64_peak):
     are lower bounds of the kernels' own rates (DESIGN.md section 3 has the
     stand-alone ncu numbers)."""
     work = stage_work(cfg, cfg.n)
-    out = {}
+    out = {"_note": "per-launch durations measured on each ID's lane stream while the other IDs in flight share "
+                    "the GPU: lower bounds of each kernel's own rate (stand-alone rates: profiles/ncu_full_r01.txt)"}
     for st, ms in stage_avg.items():
         if ms <= 0 or st not in work:
             continue
