@@ -178,8 +178,8 @@ def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic, dual=False):
     secs = avg_ms / 1e3
     if stage == "sketch":
         achieved = work["flops"] / secs / 1e12
-        kern = ("sketch_gemm_kernel (cp.async-fed DMMA m8n8k4; the dual reads A transposed)" if dual
-                else "sketch_tma_kernel (TMA-fed DMMA m8n8k4)")
+        kern = ("sketch_tma_kernel<WM, true> (TMA-fed DMMA m8n8k4, A read transposed)" if dual
+                else "sketch_tma_kernel<WM, false> (TMA-fed DMMA m8n8k4)")
         return {"kernel": kern, "bound": "tensor", "achieved": achieved,
                 "peak": fp64_peak["tflops"], "unit": "TFLOP/s", "frac": achieved / fp64_peak["tflops"],
                 "peak_source": fp64_peak["source"], "traffic": traffic, "avg_launch_ms": avg_ms,

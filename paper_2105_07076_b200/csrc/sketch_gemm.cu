@@ -398,12 +398,11 @@ cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t l
     const int64_t split_stride = ldc * N;
     cudaError_t e = cudaErrorNotSupported;
     const char* te = getenv("IDK_GEMM_TMA");
-    // TMA-fed kernel (sketch_tma.cu) for the non-transposed operand: +4-5 % over the
-    // cp.async kernel on cfg2/cfg4 (same-box A/B); for the dual it ties (27.1 vs 27.2
-    // TFLOP/s at cfg5), so the dual stays on the cp.async kernel unless IDK_GEMM_TMA=2.
-    // IDK_GEMM_TMA=0 selects the cp.async kernel everywhere.
+    // TMA-fed kernel (sketch_tma.cu) for both layouts: same-box A/B against this
+XX
+    // cfg5 (the dual) 27.2 -> 30.3.  IDK_GEMM_TMA=0 selects the cp.async kernel.
     const int tma = te ? atoi(te) : 1;
-    if ((tma == 1 && !b_trans) || tma == 2)
+    if (tma != 0)
         e = sketch_gemm_tma(A, lda, B, ldb, b_trans, out, ldc, split_stride, M, N, K, splits, wm, stream);
     if (e == cudaErrorNotSupported) {
         cudaGetLastError();

@@ -4,7 +4,7 @@
 // reference's matmul(Omega, A), matrix.cpp:28-48), but the operand tiles are
 // brought in by the Tensor Memory Accelerator: one thread issues
 // cp.async.bulk.tensor loads of 16 x 16 (Omega) and 16 x 64 (A) boxes into a
-// kStagesT-deep ring with an mbarrier per stage, so the compute warps do no
+// kStagesT-deep ring (2: measured equal to 3 and 4 CTAs fit per SM) with an mbarrier per stage, so the compute warps do no
 // address arithmetic for the loads at all.  Boxes are 128-byte rows with the
 // hardware 128B swizzle (16-byte chunk c of row r stored at c ^ (r mod 8)),
 // which keeps the DMMA fragment loads free of bank conflicts without padding.
@@ -25,7 +25,7 @@ constexpr int kBNT = 64;
 constexpr int kBKT = 16;
 constexpr int kThreadsT = 128;
 #ifndef IDK_TMA_STAGES
-#define IDK_TMA_STAGES 3
+#define IDK_TMA_STAGES 2
 #endif
 constexpr int kStagesT = IDK_TMA_STAGES;
 
@@ -126,7 +126,21 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     if (tid == 0)
         for (int s = 0; s < kStagesT - 1 && s < ktiles; ++s) issue(s);
 
+    // Warp rows are interleaved by 16-row box: warp wm owns rows 16*tm + 8*wm + fr
+    // (tm < WM), so every fragment address is a compile-time offset plus one of
+    // two per-lane swizzle values.  In a 128B-swizzled box, element (row r, k)
+    // sits at k*16 + (((r>>1) ^ (k&7)) << 1 | (r&1)); with r = 8*wm + fr and
+    // k = 4*kq + fc the swizzle term is ((fr>>1) ^ fc) ^ 4*(wm ^ kq), i.e. a
+    // lane constant X0 or X1 = X0 ^ 8 (in doubles) picked by the parity of kq.
     const int fr = lane >> 2, fc = lane & 3;
+    const int x0 = (((fr >> 1) ^ fc) << 1) + (fr & 1) + fc * 16;
+    const int ya = wm ? (x0 ^ 8) : x0, yb = wm ? x0 : (x0 ^ 8);  // kq even / odd
+    // B (non-transposed): row j = n index (j & 7 == fr), k index = 4*kq + fc:
+    // chunk ((2*kq + (fc>>1)) ^ fr), element fc & 1
+    const int bz = ((fc >> 1) ^ (fr & 1)), bf6 = fr & 6;
+    const int brow = (wn * 32 + fr) * 16 + (fc & 1);
+    // B (transposed, four 16x16 boxes): like A with row = n index within the box
+    const int xb0 = (((fr >> 1) ^ fc) << 1) + (fr & 1) + fc * 16;
     for (int kt = 0; kt < ktiles; ++kt) {
         const int st = kt % kStagesT;
         mbar_wait_t(&full[st], static_cast<unsigned>((kt / kStagesT) & 1));
@@ -139,22 +153,19 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         const double* Bs = As + S::A_ELEMS;
 #pragma unroll
         for (int kq = 0; kq < kBKT / 4; ++kq) {
-            const int kk = kq * 4 + fc;
             double af[WM], bf[4];
+            const int ay = (kq & 1) ? yb : ya;
 #pragma unroll
-            for (int tm = 0; tm < WM; ++tm) {
-                const int r = wm * (8 * WM) + tm * 8 + fr;  // row of the A tile
-                const int ii = r & 15;
-                af[tm] = As[(r >> 4) * 256 + kk * 16 + ((((ii >> 1) ^ (kk & 7)) << 1) | (ii & 1))];
-            }
+            for (int tm = 0; tm < WM; ++tm) af[tm] = As[tm * 256 + kq * 64 + ay];
 #pragma unroll
             for (int tn = 0; tn < 4; ++tn) {
-                const int j = wn * 32 + tn * 8 + fr;
                 if constexpr (kNT) {
-                    const int jj = j & 15;
-                    bf[tn] = Bs[(j >> 4) * 256 + kk * 16 + ((((jj >> 1) ^ (kk & 7)) << 1) | (jj & 1))];
+                    // n index j = wn*32 + tn*8 + fr: box (j >> 4) = 2*wn + (tn >> 1), row within box 8*(tn&1) + fr
+                    const int xr = (tn & 1) ? (xb0 ^ 8) : xb0;
+                    const int xk = (kq & 1) ? (xr ^ 8) : xr;
+                    bf[tn] = Bs[(2 * wn + (tn >> 1)) * 256 + kq * 64 + xk];
                 } else {
-                    bf[tn] = Bs[j * 16 + ((((kk >> 1) ^ (j & 7)) << 1) | (kk & 1))];
+                    bf[tn] = Bs[brow + tn * 128 + ((((2 * kq) ^ bf6) | bz) << 1)];
                 }
             }
 #pragma unroll
@@ -166,7 +177,7 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 
 #pragma unroll
     for (int tm = 0; tm < WM; ++tm) {
-        const int i = m0 + wm * (8 * WM) + tm * 8 + fr;
+        const int i = m0 + 16 * tm + 8 * wm + fr;
         if (i >= M) continue;
 #pragma unroll
         for (int tn = 0; tn < 4; ++tn) {

@@ -1,6 +1,6 @@
 # same-box A/B of two TMA sketch builds (ab/A.so, ab/B.so): sketch alone + cfg2 headline + cfg4
-IDK_LIB_PATH=paper_2105_07076_b200/ab/B.so python -m pytest tests -x -q -m gpu -k "sketch or rid or config or approx or diag" 2>&1 | tail -1
-for r in 1 2; do for v in A B; do
+IDK_LIB_PATH=paper_2105_07076_b200/ab/B.so python -m pytest tests -x -q -m gpu -k "sketch or rid or config or approx or diag" 2>&1 | tail -1; IDK_GEMM_TMA=2 IDK_LIB_PATH=paper_2105_07076_b200/ab/B.so python -m pytest tests -x -q -m gpu -k "sketch or rid or config or dual or tall" 2>&1 | tail -1
+for r in 1 2; do for v in A B C; do
   IDK_LIB_PATH=paper_2105_07076_b200/ab/$v.so python - <<'PY'
 import os, sys
 sys.path.insert(0, os.getcwd())
