@@ -398,9 +398,9 @@ cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t l
     const int64_t split_stride = ldc * N;
     cudaError_t e = cudaErrorNotSupported;
     const char* te = getenv("IDK_GEMM_TMA");
-    // TMA-fed kernel (sketch_tma.cu) for both layouts: same-box A/B against this
-XX
-    // cfg5 (the dual) 27.2 -> 30.3.  IDK_GEMM_TMA=0 selects the cp.async kernel.
+    // TMA-fed kernel (sketch_tma.cu) for both layouts; same-box A/B against this
+    // file's cp.async kernel: cfg4 29.4 -> 32.4 TFLOP/s, the dual (cfg5) 27.2 -> 30.3,
+    // cfg2 19.2 -> 20.7.  IDK_GEMM_TMA=0 selects the cp.async kernel.
     const int tma = te ? atoi(te) : 1;
     if (tma != 0)
         e = sketch_gemm_tma(A, lda, B, ldb, b_trans, out, ldc, split_stride, M, N, K, splits, wm, stream);
