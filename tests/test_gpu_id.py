@@ -233,6 +233,29 @@ def test_sketch_gemm_matches_reference_matmul(idk, ref):
         assert rel(yt, ref.matmul(om, a)) <= 1e-13
 
 
+@pytest.mark.parametrize("l,m,n", [(1, 5, 7), (7, 33, 65), (17, 2001, 130), (110, 2000, 333), (272, 300, 129),
+                                   (72, 1000, 4097), (130, 64, 64)])
+def test_tma_sketch_bit_identical_to_cp_async_kernel(idk, ref, monkeypatch, l, m, n):
+    """The TMA-fed DMMA GEMM (sketch_tma.cu: zero-filled boxes, swizzled
+    fragments) and the cp.async kernel (IDK_GEMM_TMA=0) run the same DMMA
+    sequence per output tile and the same split order: bit-identical Y, both
+    layouts, also through a padded leading dimension."""
+    import torch
+    om = ref.generate(1, l, m, 5)
+    a = ref.gaussian_matrix(m, n, 6)
+    big = torch.zeros((n, m + 6), dtype=torch.float64, device="cuda")  # lda = m + 6 (even)
+    big[:, :m] = torch.from_numpy(np.ascontiguousarray(a.T))
+    a_pad = big.t()[:m, :]
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("IDK_GEMM_TMA", mode)
+        outs[mode] = (host(idk.sketch(dev(om), dev(a))), host(idk.sketch(dev(om), dev(a.T), transposed=True)),
+                      host(idk.sketch(dev(om), a_pad)))
+    for x, y in zip(outs["1"], outs["0"]):
+        assert np.array_equal(x, y)
+    assert rel(outs["1"][0], ref.matmul(om, a)) <= 1e-13
+
+
 def test_dual_sketch_matches_reference_on_transpose(idk, ref):
     """id_auto randomized on a tall A == sketch composition on A^T, without forming A^T on the GPU."""
     a = ref.gaussian_matrix(900, 120, 31)
