@@ -43,7 +43,7 @@ struct idk_context {
     // pipelined host entry: status words land here (pinned) instead of a sync per ID
     int* async_status = nullptr;
     cudaStream_t s_in = nullptr, s_out = nullptr;
-    cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out[2] = {};
+    std::vector<cudaEvent_t> ev_io;  // pipelined host entry: in / done / out per buffer set
     int* h_status_many = nullptr;
     int64_t h_status_many_cap = 0;
     // concurrent batch entry: child contexts, one stream + workspace each
@@ -62,6 +62,8 @@ struct idk_context {
 };
 
 namespace {
+
+int ensure_lanes(idk_context* h, int L);  // lane contexts of the concurrent entries (defined below)
 
 constexpr size_t kAlign = 256;
 
@@ -584,11 +586,7 @@ int idk_destroy(idk_handle h) {
     if (h->h_status_many) cudaFreeHost(h->h_status_many);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
-    for (int i = 0; i < 2; ++i) {
-        if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
-        if (h->ev_done[i]) cudaEventDestroy(h->ev_done[i]);
-        if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
-    }
+    for (cudaEvent_t e : h->ev_io) cudaEventDestroy(e);
     if (h->s_in) cudaStreamDestroy(h->s_in);
     if (h->s_out) cudaStreamDestroy(h->s_out);
     delete h;
@@ -928,10 +926,17 @@ int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a,
     const bool tall = m > n;
     const int64_t zc = tall ? m : n, crow = tall ? n : m;
     const bool want_c = h_c != nullptr;
-    // two buffer sets: ID i+1's upload overlaps ID i's compute and ID i-1's download
+    // Computes run on L lane contexts (one stream each, as idk_id_auto_batch),
+    // so IDs whose device time exceeds their transfer time (small matrices:
+    // cfg1) overlap on the GPU; uploads stay in order on s_in and downloads on
+    // s_out.  S = 2L buffer sets: ID i+L's upload overlaps ID i's compute.
+    int L = static_cast<int>(std::min<int64_t>({h->lanes, 8, count}));
+    if (const char* e = getenv("IDK_HOST_LANES")) L = std::max(1, std::min(L, atoi(e)));  // tuning only
+    const int S = 2 * L;
+    if ((rc = ensure_lanes(h, L))) return rc;
     Carve cv;
-    size_t aofs[2], cofs[2], zofs[2], ccofs[2];
-    for (int b = 0; b < 2; ++b) {
+    std::vector<size_t> aofs(S), cofs(S), zofs(S), ccofs(S);
+    for (int b = 0; b < S; ++b) {
         aofs[b] = cv.take(sizeof(double) * m * n);
         cofs[b] = cv.take(sizeof(int64_t) * k);
         zofs[b] = cv.take(sizeof(double) * k * zc);
@@ -941,12 +946,15 @@ int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a,
     if (!h->s_in) {
         IDK_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
         IDK_CUDA(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
-        for (int b = 0; b < 2; ++b) {
-            IDK_CUDA(cudaEventCreateWithFlags(&h->ev_in[b], cudaEventDisableTiming));
-            IDK_CUDA(cudaEventCreateWithFlags(&h->ev_done[b], cudaEventDisableTiming));
-            IDK_CUDA(cudaEventCreateWithFlags(&h->ev_out[b], cudaEventDisableTiming));
-        }
     }
+    while (static_cast<int>(h->ev_io.size()) < 3 * S) {
+        cudaEvent_t e;
+        IDK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_io.push_back(e);
+    }
+    cudaEvent_t* ev_in = h->ev_io.data();
+    cudaEvent_t* ev_done = ev_in + S;
+    cudaEvent_t* ev_out = ev_done + S;
     if (count > h->h_status_many_cap) {
         if (h->h_status_many) cudaFreeHost(h->h_status_many);
         h->h_status_many = nullptr;
@@ -954,37 +962,55 @@ int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a,
         IDK_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h->h_status_many), sizeof(int) * count));
         h->h_status_many_cap = count;
     }
-    const bool prof = h->profiling;
-    h->profiling = false;
+    // work already queued on the handle's stream precedes every lane and copy
+    if (!h->ev_fork) IDK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    IDK_CUDA(cudaEventRecord(h->ev_fork, h->stream));
+    IDK_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_fork, 0));
+    for (int l = 0; l < L; ++l) {
+        idk_context* kid = h->kids[static_cast<size_t>(l)];
+        kid->cpqr_mode = h->cpqr_mode;
+        kid->batched_exact = h->batched_exact;
+        kid->profiling = false;
+        IDK_CUDA(cudaStreamWaitEvent(kid->stream, h->ev_fork, 0));
+    }
+    int64_t launched = 0;
     for (int64_t i = 0; i < count; ++i) {
-        const int b = static_cast<int>(i & 1);
+        const int b = static_cast<int>(i % S);
+        idk_context* kid = h->kids[static_cast<size_t>(i % L)];
         double* d_a = reinterpret_cast<double*>(h->io + aofs[b]);
         int64_t* d_cols = reinterpret_cast<int64_t*>(h->io + cofs[b]);
         double* d_z = reinterpret_cast<double*>(h->io + zofs[b]);
         double* d_c = want_c ? reinterpret_cast<double*>(h->io + ccofs[b]) : nullptr;
-        if (i >= 2) IDK_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_out[b], 0));  // set b fully drained
+        if (i >= S) IDK_CUDA(cudaStreamWaitEvent(h->s_in, ev_out[b], 0));  // set b fully drained
         IDK_CUDA(cudaMemcpyAsync(d_a, h_a[i], sizeof(double) * m * n, cudaMemcpyHostToDevice, h->s_in));
-        IDK_CUDA(cudaEventRecord(h->ev_in[b], h->s_in));
-        IDK_CUDA(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0));
+        IDK_CUDA(cudaEventRecord(ev_in[b], h->s_in));
+        IDK_CUDA(cudaStreamWaitEvent(kid->stream, ev_in[b], 0));
         h->h_status_many[i] = 0x7f7f7f7f;
-        h->async_status = h->h_status_many + i;
-        rc = id_auto_dev(h, d_a, m, n, m, k, method, seed, p, omega_mode, nullptr, d_cols, d_z, d_c, transposed);
-        h->async_status = nullptr;
+        kid->async_status = h->h_status_many + i;
+        const int64_t before = kid->launches;
+        rc = id_auto_dev(kid, d_a, m, n, m, k, method, seed, p, omega_mode, nullptr, d_cols, d_z, d_c, transposed);
+        kid->async_status = nullptr;
+        launched += kid->launches - before;
         if (rc) {
-            h->profiling = prof;
-            cudaStreamSynchronize(h->stream);
+            rc = set_err(h, rc, kid->err);
+            for (int l = 0; l < L; ++l) cudaStreamSynchronize(h->kids[static_cast<size_t>(l)]->stream);
+            cudaStreamSynchronize(h->s_in);
+            cudaStreamSynchronize(h->s_out);
+            h->launches += launched;
             return rc;
         }
-        IDK_CUDA(cudaEventRecord(h->ev_done[b], h->stream));
-        IDK_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_done[b], 0));
+        IDK_CUDA(cudaEventRecord(ev_done[b], kid->stream));
+        IDK_CUDA(cudaStreamWaitEvent(h->s_out, ev_done[b], 0));
         IDK_CUDA(cudaMemcpyAsync(h_cols[i], d_cols, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->s_out));
         IDK_CUDA(cudaMemcpyAsync(h_z[i], d_z, sizeof(double) * k * zc, cudaMemcpyDeviceToHost, h->s_out));
         if (want_c) IDK_CUDA(cudaMemcpyAsync(h_c[i], d_c, sizeof(double) * crow * k, cudaMemcpyDeviceToHost, h->s_out));
-        IDK_CUDA(cudaEventRecord(h->ev_out[b], h->s_out));
+        IDK_CUDA(cudaEventRecord(ev_out[b], h->s_out));
     }
-    h->profiling = prof;
+    h->launches += launched;
+    // the handle's stream waits for everything (callers time on it)
+    IDK_CUDA(cudaEventRecord(ev_out[(count - 1) % S], h->s_out));
+    IDK_CUDA(cudaStreamWaitEvent(h->stream, ev_out[(count - 1) % S], 0));
     IDK_CUDA(cudaStreamSynchronize(h->stream));
-    IDK_CUDA(cudaStreamSynchronize(h->s_out));
     for (int64_t i = 0; i < count; ++i) {
         const int bad = h->h_status_many[i];
         if (bad != 0x7f7f7f7f) {
@@ -1000,6 +1026,33 @@ int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a,
 }  // extern "C"
 
 namespace {
+
+// Lane contexts of the concurrent entries: one non-blocking, highest-priority
+// stream and one grow-only workspace each (created on first use, kept).
+int ensure_lanes(idk_context* h, int L) {
+    while (static_cast<int>(h->kids.size()) < L) {
+        idk_context* kid = nullptr;
+        int rc = idk_create(&kid, h->device);
+        if (rc) return set_err(h, rc, "lane context creation failed");
+        cudaStream_t ks;
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        const char* pe = getenv("IDK_LANE_PRIO");
+        if (pe && atoi(pe) == 0) hi = 0;
+        // lanes run the latency-bound CPQRs: highest priority, so their clusters
+        // are dispatched ahead of the (low-priority) grouped sketch CTAs
+        if (cudaStreamCreateWithPriority(&ks, cudaStreamNonBlocking, hi) != cudaSuccess) {
+            idk_destroy(kid);
+            return set_err(h, IDK_ERR_CUDA, "lane stream creation failed");
+        }
+        kid->stream = ks;
+        h->kids.push_back(kid);
+        cudaEvent_t e;
+        IDK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_join.push_back(e);
+    }
+    return IDK_OK;
+}
 
 // Grouped batch of sketch RIDs (idk_id_auto_batch, method 1, Philox Omega):
 // the Omegas and sketches of `chunk` IDs at a time run as ONE Omega launch and
@@ -1124,26 +1177,8 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
     if (count == 0) return IDK_OK;
     // child contexts: one non-blocking stream and one workspace per lane
     const int L = static_cast<int>(std::min<int64_t>(h->lanes, count));
-    while (static_cast<int>(h->kids.size()) < L) {
-        idk_context* kid = nullptr;
-        if ((rc = idk_create(&kid, h->device))) return set_err(h, rc, "id_auto_batch: lane context creation failed");
-        cudaStream_t ks;
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        const char* pe = getenv("IDK_LANE_PRIO");
-        if (pe && atoi(pe) == 0) hi = 0;
-        // lanes run the latency-bound CPQRs: highest priority, so their clusters
-        // are dispatched ahead of the (low-priority) grouped sketch CTAs
-        if (cudaStreamCreateWithPriority(&ks, cudaStreamNonBlocking, hi) != cudaSuccess) {
-            idk_destroy(kid);
-            return set_err(h, IDK_ERR_CUDA, "id_auto_batch: stream creation failed");
-        }
-        kid->stream = ks;
-        h->kids.push_back(kid);
-        cudaEvent_t e;
-        IDK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        h->ev_join.push_back(e);
-    }
+    if ((rc = ensure_lanes(h, L))) return rc;
+    if (!h->ev_fork) IDK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     if (!h->ev_fork) IDK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     if (count > h->h_status_many_cap) {
         if (h->h_status_many) cudaFreeHost(h->h_status_many);
