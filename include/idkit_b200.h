@@ -159,6 +159,15 @@ IDK_API int idk_id_auto(idk_handle h, const double* d_a, int64_t m, int64_t n, i
 IDK_API int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t m, int64_t n, int64_t lda,
                          int64_t stride, int64_t k, int64_t* d_cols, double* d_z, double* d_c);
 
+/* Host-buffer form of idk_optim_id_batched (value semantics of optim_id,
+ * id.hpp:40, per matrix): h_a holds batch packed column-major m x n matrices
+ * (stride m*n), outputs packed as in the device entry.  Chunks of
+ * 2 x num_SMs matrices are uploaded, factored and downloaded in a pipeline
+ * (upload of chunk c+1 and download of chunk c-1 overlap the kernel of chunk
+ * c); pinned host buffers make the copies asynchronous. */
+IDK_API int idk_optim_id_batched_host(idk_handle h, const double* h_a, int64_t batch, int64_t m, int64_t n, int64_t k,
+                                      int64_t* h_cols, double* h_z, double* h_c);
+
 /* Sharded entry: the caller all-gathered the sketch Y
  * (l x n, ldy) of a column-sharded A; factor it (CPQR, identical on every
  * rank: deterministic) and solve Z only for its own columns [c_begin, c_end)

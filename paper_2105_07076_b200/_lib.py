@@ -41,6 +41,7 @@ SIGNATURES = {
     "idk_id_auto": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P, _P,
                               C.POINTER(C.c_int)]),
     "idk_optim_id_batched": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P]),
+    "idk_optim_id_batched_host": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "idk_id_from_sketch": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P]),
     "idk_sketch_omega": (C.c_int, [_P, _I64, _I64, C.c_uint64, _P]),
     "idk_sketch": (C.c_int, [_P, _P, _I64, _P, _I64, _I64, _I64, C.c_int, _P, _I64]),

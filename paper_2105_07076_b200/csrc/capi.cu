@@ -42,6 +42,7 @@ struct idk_context {
     bool batched_exact = false;
     // pipelined host entry: status words land here (pinned) instead of a sync per ID
     int* async_status = nullptr;
+    int* batched_status = nullptr;  // idk_optim_id_batched_host: device status words of the current chunk
     cudaStream_t s_in = nullptr, s_out = nullptr;
     std::vector<cudaEvent_t> ev_io;  // pipelined host entry: in / done / out per buffer set
     int* h_status_many = nullptr;
@@ -700,10 +701,13 @@ int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t
     if (!fast && idk::batched_id_smem_bytes(static_cast<int>(m), static_cast<int>(n)) > h->smem_optin)
         return set_err(h, IDK_ERR_INVALID_ARG, "optim_id_batched: m x n too large for one CTA's shared memory");
     if (batch == 0) return IDK_OK;
-    Carve cv;
-    const size_t sofs = cv.take(sizeof(int) * batch);
-    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
-    int* status = reinterpret_cast<int*>(h->ws + sofs);
+    int* status = h->batched_status;  // device status words supplied by idk_optim_id_batched_host
+    if (!status) {
+        Carve cv;
+        const size_t sofs = cv.take(sizeof(int) * batch);
+        if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+        status = reinterpret_cast<int*>(h->ws + sofs);
+    }
     if (fast)
         IDK_CUDA(idk::batched_id_fast(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n),
                                       static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
@@ -713,6 +717,90 @@ int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t
                                  static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
                                  h->stream));
     h->launches += 1;
+    if (h->batched_status) return IDK_OK;  // idk_optim_id_batched_host checks the statuses itself
+    std::vector<int> st(static_cast<size_t>(batch));
+    IDK_CUDA(cudaMemcpyAsync(st.data(), status, sizeof(int) * batch, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    for (int64_t b = 0; b < batch; ++b)
+        if (st[b] >= 0)
+            return set_err(h, IDK_ERR_NOT_POSDEF, "optim_id_batched: matrix " + std::to_string(b) +
+                                                      " is rank deficient (R11 diagonal " + std::to_string(st[b]) +
+                                                      " is zero)");
+    return IDK_OK;
+}
+
+int idk_optim_id_batched_host(idk_handle h, const double* h_a, int64_t batch, int64_t m, int64_t n, int64_t k,
+                              int64_t* h_cols, double* h_z, double* h_c) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (batch < 0 || (batch > 0 && (!h_a || !h_cols || !h_z)))
+        return set_err(h, IDK_ERR_INVALID_ARG, "optim_id_batched_host: bad arguments");
+    int rc = check_k(h, m, n, k, "optim_id_batched");
+    if (rc) return rc;
+    if (batch == 0) return IDK_OK;
+    // chunks of 2 x num_sms matrices through 3 buffer sets: chunk c+1 uploads
+    // while chunk c factors and chunk c-1 downloads
+    const int64_t chunk = std::min<int64_t>(batch, 2LL * h->num_sms);
+    const int64_t nchunks = (batch + chunk - 1) / chunk;
+    constexpr int S = 3;
+    const int64_t mn = m * n;
+    Carve cv;
+    size_t aofs[S], cofs[S], zofs[S], ccofs[S];
+    for (int b = 0; b < S; ++b) {
+        aofs[b] = cv.take(sizeof(double) * mn * chunk);
+        cofs[b] = cv.take(sizeof(int64_t) * k * chunk);
+        zofs[b] = cv.take(sizeof(double) * k * n * chunk);
+        ccofs[b] = cv.take(sizeof(double) * m * k * chunk);
+    }
+    const size_t sofs = cv.take(sizeof(int) * batch);
+    if ((rc = ensure(h, &h->io, &h->io_cap, cv.total))) return rc;
+    if (!h->s_in) {
+        IDK_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+        IDK_CUDA(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    }
+    while (static_cast<int>(h->ev_io.size()) < 3 * S) {
+        cudaEvent_t e;
+        IDK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_io.push_back(e);
+    }
+    cudaEvent_t* ev_in = h->ev_io.data();
+    cudaEvent_t* ev_done = ev_in + S;
+    cudaEvent_t* ev_out = ev_done + S;
+    if (!h->ev_fork) IDK_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    IDK_CUDA(cudaEventRecord(h->ev_fork, h->stream));
+    IDK_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_fork, 0));
+    int* status = reinterpret_cast<int*>(h->io + sofs);
+    const bool want_c = h_c != nullptr;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int b = static_cast<int>(c % S);
+        const int64_t b0 = c * chunk, cnt = std::min<int64_t>(chunk, batch - b0);
+        double* d_a = reinterpret_cast<double*>(h->io + aofs[b]);
+        int64_t* d_cols = reinterpret_cast<int64_t*>(h->io + cofs[b]);
+        double* d_z = reinterpret_cast<double*>(h->io + zofs[b]);
+        double* d_c = want_c ? reinterpret_cast<double*>(h->io + ccofs[b]) : nullptr;
+        if (c >= S) IDK_CUDA(cudaStreamWaitEvent(h->s_in, ev_out[b], 0));
+        IDK_CUDA(cudaMemcpyAsync(d_a, h_a + b0 * mn, sizeof(double) * mn * cnt, cudaMemcpyHostToDevice, h->s_in));
+        IDK_CUDA(cudaEventRecord(ev_in[b], h->s_in));
+        IDK_CUDA(cudaStreamWaitEvent(h->stream, ev_in[b], 0));
+        h->batched_status = status + b0;
+        rc = idk_optim_id_batched(h, d_a, cnt, m, n, m, mn, k, d_cols, d_z, d_c);
+        h->batched_status = nullptr;
+        if (rc) {
+            cudaStreamSynchronize(h->stream);
+            cudaStreamSynchronize(h->s_in);
+            cudaStreamSynchronize(h->s_out);
+            return rc;
+        }
+        IDK_CUDA(cudaEventRecord(ev_done[b], h->stream));
+        IDK_CUDA(cudaStreamWaitEvent(h->s_out, ev_done[b], 0));
+        IDK_CUDA(cudaMemcpyAsync(h_cols + b0 * k, d_cols, sizeof(int64_t) * k * cnt, cudaMemcpyDeviceToHost, h->s_out));
+        IDK_CUDA(cudaMemcpyAsync(h_z + b0 * k * n, d_z, sizeof(double) * k * n * cnt, cudaMemcpyDeviceToHost, h->s_out));
+        if (want_c)
+            IDK_CUDA(cudaMemcpyAsync(h_c + b0 * m * k, d_c, sizeof(double) * m * k * cnt, cudaMemcpyDeviceToHost,
+                                     h->s_out));
+        IDK_CUDA(cudaEventRecord(ev_out[b], h->s_out));
+    }
+    IDK_CUDA(cudaStreamWaitEvent(h->stream, ev_out[(nchunks - 1) % S], 0));
     std::vector<int> st(static_cast<size_t>(batch));
     IDK_CUDA(cudaMemcpyAsync(st.data(), status, sizeof(int) * batch, cudaMemcpyDeviceToHost, h->stream));
     IDK_CUDA(cudaStreamSynchronize(h->stream));

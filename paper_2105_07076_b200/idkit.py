@@ -380,8 +380,24 @@ def matmul_ref(a, b):
 def optim_id_batched(a, k: int, want_c: bool = True):
     """BASELINE cfg3: `a` is a (batch, n, m) contiguous CUDA tensor holding
     batch column-major m x n matrices (i.e. a[b].t() is matrix b).
-    Returns cols (batch, k), z (batch, n, k) [= Z_b^T row-major], c (batch, k, m)."""
+    Returns cols (batch, k), z (batch, n, k) [= Z_b^T row-major], c (batch, k, m).
+    A numpy array (or CPU tensor) of the same layout runs through the pipelined
+    host entry (idk_optim_id_batched_host) and returns numpy arrays."""
     import torch
+    if not is_torch(a) or a.device.type == "cpu":
+        import numpy as np
+        ah = a.numpy() if is_torch(a) else np.asarray(a)
+        if ah.ndim != 3 or ah.dtype != np.float64:
+            raise InvalidArgument("batched input must be a (batch, n, m) fp64 array")
+        ah = np.ascontiguousarray(ah)
+        batch, n, m = ah.shape
+        ctx = context(0)
+        cols = np.empty((batch, max(k, 0)), dtype=np.int64)
+        z = np.empty((batch, n, max(k, 0)), dtype=np.float64)
+        c = np.empty((batch, max(k, 0), m), dtype=np.float64) if want_c else None
+        ctx.check(ctx.lib.idk_optim_id_batched_host(ctx.h, ah.ctypes.data, batch, m, n, k, cols.ctypes.data,
+                                                    z.ctypes.data, c.ctypes.data if want_c else None))
+        return cols, z, c
     if a.dim() != 3 or not a.is_contiguous() or a.dtype != torch.float64:
         raise InvalidArgument("batched input must be a contiguous (batch, n, m) fp64 tensor")
     batch, n, m = a.shape

@@ -413,3 +413,22 @@ def test_grouped_sketch_batch_matches_single_calls(idk, oracle, monkeypatch, chu
             assert np.array_equal(host(c_), host(r.cols))
             assert np.array_equal(host(z_), host(r.z))
             assert np.array_equal(host(cc), host(r.c))
+
+
+def test_batched_host_entry_matches_device_entry(idk, oracle):
+    """idk_optim_id_batched_host (chunks of 2 x num_SMs matrices through a
+    3-deep upload / factor / download pipeline) returns exactly the device
+    entry's results, across chunk boundaries; a rank-deficient matrix in a
+    later chunk is reported with its batch index."""
+    import torch
+    from paper_2105_07076_b200.configs import make_np
+    a = make_np("cfg3", seed=21, scale=700 / 4096)  # (700, n, m): 3 chunks on a 148-SM B200
+    cols_h, z_h, c_h = idk.optim_id_batched(a, 16)
+    cols_d, z_d, c_d = idk.optim_id_batched(torch.from_numpy(a).cuda(), 16)
+    assert np.array_equal(cols_h, host(cols_d))
+    assert np.array_equal(z_h, host(z_d))
+    assert np.array_equal(c_h, host(c_d))
+    bad = a.copy()
+    bad[650] = 0.0
+    with pytest.raises(idk.NotPositiveDefiniteError, match="matrix 650"):
+        idk.optim_id_batched(bad, 16)
