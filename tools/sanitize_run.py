@@ -26,5 +26,14 @@ ctx.set_batched_exact(True)
 idk.optim_id_batched(b, 16)
 ctx.set_batched_exact(False)
 idk.id_auto_batch([dev(rng.standard_normal((60, 90))) for _ in range(5)], 8, idk.RANDOMIZED, p=3, lanes=3)
+# TMA sketch (both layouts, partial boxes), DMMA Z solves (k <= 128 and 128 < k <= 256), both gathers,
+# the pipelined host entries
+idk.sketch_rid(dev(rng.standard_normal((900, 150))), 20, 6, seed=5)            # dual: TMA with A transposed
+idk.sketch_rid(dev(rng.standard_normal((170, 1100))), 150, 10, seed=6)         # k in (128, 256]
+idk.optim_id(dev(rng.standard_normal((140, 333))), 100)
+idk.select_columns(dev(rng.standard_normal((64, 300))), torch.arange(0, 40, 3).cuda())
+idk.select_columns(dev(rng.standard_normal((301, 77))), torch.arange(0, 40, 3).cuda(), rows_of_a=True)
+idk.id_auto_many([np.asfortranarray(rng.standard_normal((60, 90))) for _ in range(5)], 8, idk.RANDOMIZED, p=3)
+idk.optim_id_batched(rng.standard_normal((300, 256, 64)), 16)
 torch.cuda.synchronize()
 print("sanitize run ok")
