@@ -145,14 +145,17 @@ void idko_philox4x32_10(uint32_t c[4], const uint32_t key[2]) {
 void idko_omega_philox(int64_t l, int64_t m, uint64_t seed, double* out) {
     const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     const int64_t total = l * m;
-    for (int64_t e = 0; e < total; ++e) {
-        uint32_t c[4] = {(uint32_t)e, (uint32_t)((uint64_t)e >> 32), 0u, 0u};
+    /* element pair (2j, 2j+1) <- Philox block j: the Box-Muller (cos, sin) pair */
+    for (int64_t j = 0; 2 * j < total; ++j) {
+        uint32_t c[4] = {(uint32_t)j, (uint32_t)((uint64_t)j >> 32), 0u, 0u};
         idko_philox4x32_10(c, key);
         const uint64_t r1 = ((uint64_t)c[1] << 32) | c[0];
         const uint64_t r2 = ((uint64_t)c[3] << 32) | c[2];
         const double u1 = (double)((r1 >> 11) + 1) * 0x1.0p-53;
         const double u2 = (double)(r2 >> 11) * 0x1.0p-53;
-        out[e] = sqrt(-2.0 * log(u1)) * cos(2.0 * kPi * u2);
+        const double r = sqrt(-2.0 * log(u1)), th = 2.0 * kPi * u2;
+        out[2 * j] = r * cos(th);
+        if (2 * j + 1 < total) out[2 * j + 1] = r * sin(th);
     }
 }
 

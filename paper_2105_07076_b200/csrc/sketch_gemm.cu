@@ -495,19 +495,24 @@ cudaError_t gemm_residual(const double* A, int64_t lda, const double* B, int64_t
 
 namespace idk {
 namespace {
+__device__ __forceinline__ void omega_pairs(double* __restrict__ out, int64_t total, uint64_t seed) {
+    const int64_t pairs = (total + 1) / 2;
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < pairs;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double c0, c1;
+        philox_normal_pair(static_cast<uint64_t>(j), seed, c0, c1);
+        out[2 * j] = c0;
+        if (2 * j + 1 < total) out[2 * j + 1] = c1;
+    }
+}
+
 __global__ void omega_philox_kernel(double* __restrict__ out, int64_t total, uint64_t seed) {
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[e] = philox_normal(static_cast<uint64_t>(e), seed);
+    omega_pairs(out, total, seed);
 }
 
 // One Omega per group member (blockIdx.y), member g at out + g*total.
 __global__ void omega_philox_group_kernel(double* __restrict__ out, int64_t total, const GroupSeeds seeds) {
-    const uint64_t seed = seeds.s[blockIdx.y];
-    out += blockIdx.y * total;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[e] = philox_normal(static_cast<uint64_t>(e), seed);
+    omega_pairs(out + blockIdx.y * total, total, seeds.s[blockIdx.y]);
 }
 }  // namespace
 
@@ -524,7 +529,7 @@ cudaError_t omega_philox_group(double* out, int64_t l, int64_t m, const GroupSee
 cudaError_t omega_philox(double* out, int64_t l, int64_t m, uint64_t seed, cudaStream_t stream) {
     const int64_t total = l * m;
     if (total <= 0) return cudaSuccess;
-    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    const int blocks = static_cast<int>(std::min<int64_t>((total / 2 + 255) / 256 + 1, 148 * 8));
     omega_philox_kernel<<<blocks, 256, 0, stream>>>(out, total, seed);
     return cudaGetLastError();
 }
