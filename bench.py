@@ -3,11 +3,11 @@
 
 Default workload (N=1): BASELINE configs[1] ("cfg2"): Gaussian-sketch RID of a
 2000 x 4000 fp64 A = U diag(exp(-i/30)) V^T, k = 100, p = 10, Omega from the
-on-device Philox generator.  A "step" is 48 distinct cfg2 IDs (sketch -> CPQR
+on-device Philox generator.  A "step" is 64 distinct cfg2 IDs (sketch -> CPQR
 -> Z -> C each) in flight at once through the C ABI's concurrent entry
 (idk_id_auto_batch: one stream per ID), inputs already resident in HBM
 (`--batch 1`: one ID per step through idk_id_auto).  L2 (126 MB) is flushed
-with a 256 MiB memset between timed steps (the 48 inputs are 3 GB); only the
+with a 256 MiB memset between timed steps (the 64 inputs are 4 GB); only the
 step itself is inside the CUDA events.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1..cfg5]
@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--shard", action="store_true", help="cfg4/cfg5: use the sharded layer even at N=1")
     ap.add_argument("--batch", type=int, default=None,
                     help="cfg1/cfg2: distinct matrices per step, run concurrently through idk_id_auto_batch "
-                         "(default 48 -- throughput rises with IDs in flight: 16 -> 6.06k, 48 -> 6.56k IDs/s at cfg2, profiles/inflight_r01.txt; 1 = one ID per step through idk_id_auto)")
+                         "(default 64, the lane limit of idk_set_concurrency -- throughput rises with IDs in flight: 48 -> 7.25k, 64 -> 7.36k IDs/s at cfg2, profiles/inflight_r01.txt; 1 = one ID per step through idk_id_auto)")
     return ap.parse_args()
 
 
@@ -226,7 +226,7 @@ def run_ours(args):
     # ---- inputs (harness; not timed) ----
     seed = args.seed + (rank if replicas else 0)
     a = make_torch(cfg.name, seed=seed, device=f"cuda:{local}")
-    nb = (args.batch if args.batch is not None else 48) if replicas else 1
+    nb = (args.batch if args.batch is not None else 64) if replicas else 1
     # a stream of distinct IDs: B different matrices of the same construction
     mats = [a] + [make_torch(cfg.name, seed=seed + 1000 * j, device=f"cuda:{local}") for j in range(1, nb)]
     tall = cfg.m > cfg.n
