@@ -75,7 +75,7 @@ def launches():
         a[1] += v
     tot = sum(v[1] for v in agg.values())
     lines = ["ncu launch list (gpu__time_duration.sum, --clock-control none, serialised by ncu) of "
-             "`python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e` (cfg2, 48 IDs per step), "
+             "`python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e` (cfg2, 64 IDs per step), "
              "our kernels only (-k filter in tools/gpu_profiles.sh):",
              f"{'kernel':58s} {'launches':>8s} {'total us':>10s} {'avg us':>9s} {'share':>6s}"]
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
