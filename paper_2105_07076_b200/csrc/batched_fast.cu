@@ -175,6 +175,7 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
     __shared__ double s_pa, s_sc[3];
     __shared__ int s_piv[KM];
     __shared__ int s_ppos;
+    __shared__ double s_rinv[KM];  // 1 / R11(i,i) for the Z solve
 
     const int c = threadIdx.x, lane = c & 31, wid = c >> 5;
     const bool mine = c < n;
@@ -287,9 +288,12 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
                 }
             }
         }
+        if (c < k) s_rinv[c] = 1.0 / r11[c * KM + c];
         __syncthreads();
 
-        // ---- T = R11^-1 R12 per column (solve.cpp:43-51), Z staged in smem ----
+        // ---- T = R11^-1 R12 per column (solve.cpp:43-51), Z staged in smem;
+        // the diagonal's reciprocal is formed once per matrix (a multiply per
+        // element instead of a division: within rounding of the reference) ----
         if (mine) {
             if (pos >= k) {
 #pragma unroll
@@ -299,7 +303,7 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
 #pragma unroll
                         for (int l = i + 1; l < KM; ++l)
                             if (l < k) acc = fma(-r11[l * KM + i], y[l], acc);
-                        y[i] = acc / r11[i * KM + i];
+                        y[i] = acc * s_rinv[i];
                     }
                 }
             }
