@@ -7,8 +7,11 @@
 //   * the next matrix streams into shared memory by TMA bulk copies
 //     (cp.async.bulk + mbarrier) while the current one is factored, so HBM
 //     traffic overlaps the FP64 work;
-//   * FMA arithmetic and the reflector's v kept in shared memory between zero
-//     guard rows, so the update loops have no predicates;
+//   * FMA arithmetic; the pivot column itself is the reflector source in
+//     shared memory: v = scale * column below the diagonal, with scale folded
+//     into the dot and the axpy weight, so a step has one barrier after the
+//     pivot's publish (no separate v pass) and the update loops have static
+//     bounds (no predicates);
 //   * the pivot rule is exact (lowest position among sqrt(live) >=
 //     (1-1e-14) sqrt(max)); positions replay the reference's swaps;
 //   * Z is staged in shared memory and written coalesced.
@@ -84,24 +87,25 @@ __device__ __forceinline__ double lds_v(const double* p) {
     return v;
 }
 
-// Trailing update of one non-pivot column at compile-time step S: dot with v
-// (rows S..M-1), axpy, downdate, recompute, next-step partials -- every loop
+// Trailing update of one non-pivot column at compile-time step S: dot with
+// v = [1; scale * p] (p = the pivot column below row S), axpy, downdate,
+// recompute, next-step partials -- every loop
 // has static bounds, so no predicates and no retired rows are touched.  The
 // reflector values are read 8 at a time (lds_v) so the register-resident
 // column is not spilled.
 template <int M, int S>
-__device__ __forceinline__ void column_step(double (&y)[M], const double* __restrict__ vfull, double tau,
-                                            double& live, double& anchor, double& pa, double& pt) {
+__device__ __forceinline__ void column_step(double (&y)[M], const double* __restrict__ pcol, double tau,
+                                            double scale, double& live, double& anchor, double& pa, double& pt) {
     const double ys = y[S];
     double head = ys;
     if (tau != 0.0) {
-        double d0 = ys, d1 = 0.0, d2 = 0.0, d3 = 0.0;  // v_S = 1
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;  // rows below S; v_S = 1 added after
 #pragma unroll
         for (int i0 = S + 1; i0 < M; i0 += 8) {
             double v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (i0 + u < M) v[u] = lds_v(vfull + i0 + u);
+                if (i0 + u < M) v[u] = lds_v(pcol + i0 + u);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 if (i0 + u < M) {
@@ -112,17 +116,18 @@ __device__ __forceinline__ void column_step(double (&y)[M], const double* __rest
                 }
             }
         }
-        const double w = mul_rn((d0 + d1) + (d2 + d3), tau);
+        const double w = mul_rn(fma(scale, (d0 + d1) + (d2 + d3), ys), tau);
+        const double ws = mul_rn(w, scale);
         y[S] = ys - w;
 #pragma unroll
         for (int i0 = S + 1; i0 < M; i0 += 8) {
             double v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (i0 + u < M) v[u] = lds_v(vfull + i0 + u);
+                if (i0 + u < M) v[u] = lds_v(pcol + i0 + u);
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (i0 + u < M) y[i0 + u] = fma(-w, v[u], y[i0 + u]);
+                if (i0 + u < M) y[i0 + u] = fma(-ws, v[u], y[i0 + u]);
         }
         head = ys - w;
     }
@@ -143,16 +148,6 @@ __device__ __forceinline__ void column_step(double (&y)[M], const double* __rest
     live = lv;
 }
 
-// The pivot column becomes [R; beta; v] (the reference's work layout).
-template <int M, int S>
-__device__ __forceinline__ void pivot_step(double (&y)[M], const double* __restrict__ vfull, double tau, double beta) {
-    if (tau != 0.0) {
-        y[S] = beta;
-#pragma unroll
-        for (int i = S + 1; i < M; ++i) y[i] = vfull[i];
-    }
-}
-
 #define IDK_REP32(M) \
     M(0) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) \
     M(16) M(17) M(18) M(19) M(20) M(21) M(22) M(23) M(24) M(25) M(26) M(27) M(28) M(29) M(30) M(31)
@@ -165,14 +160,13 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
     constexpr int LDS = M + 2;  // 16-byte aligned column stride; lane stride 2 banks apart
     extern __shared__ __align__(128) double sm[];
     double* stage = sm;                                   // n * LDS (TMA target)
-    double* colbuf = stage + static_cast<size_t>(n) * LDS;  // M: the pivot column as it stands
-    double* vfull = colbuf + M;                           // M: reflector by row (0 above s, 1 at s)
-    double* r11 = vfull + M;                              // KM x KM, column-major
+    double* colbuf = stage + static_cast<size_t>(n) * LDS;  // M: the pivot column as it stands (v / scale below s)
+    double* r11 = colbuf + 2 * M;                         // KM x KM, column-major
     double* zst = r11 + KM * KM;                          // k * n staging for Z
     __shared__ uint64_t bar;
     __shared__ double red_d[8];
     __shared__ unsigned red_u[8];
-    __shared__ double s_pa, s_sc[3];
+    __shared__ double s_sc[3];
     __shared__ int s_piv[KM];
     __shared__ int s_ppos;
     __shared__ double s_rinv[KM];  // 1 / R11(i,i) for the Z solve
@@ -236,6 +230,9 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
             if (piv) {  // publish the pivot column and its reflector (qr.cpp:16-28)
 #pragma unroll
                 for (int i = 0; i < M; ++i) colbuf[i] = y[i];
+#pragma unroll
+                for (int i = 0; i < KM; ++i)  // R(0..s-1, s) of this column
+                    if (i < s) r11[s * KM + i] = y[i];
                 const int len = m - s;
                 double tau = 0.0, beta = pa, scale = 1.0;
                 if (len > 1 && pt != 0.0) {
@@ -243,42 +240,24 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
                     tau = (beta - pa) / beta;
                     scale = 1.0 / (pa - beta);
                 }
-                s_pa = pa;
                 s_sc[0] = tau;
                 s_sc[1] = beta;
                 s_sc[2] = scale;
                 s_piv[s] = c;
                 s_ppos = pos;
+                r11[s * KM + s] = tau != 0.0 ? beta : pa;
             }
             __syncthreads();
-            const double alpha = s_pa, tau = s_sc[0], beta = s_sc[1], scale = s_sc[2];
-            if (c < M) {
-                const double v = c < s ? 0.0 : (c == s ? 1.0 : (c < m ? (tau != 0.0 ? mul_rn(colbuf[c], scale)
-                                                                                    : colbuf[c]) : 0.0));
-                vfull[c] = v;
-                if (c < KM && c <= s) r11[s * KM + c] = c < s ? colbuf[c] : (tau != 0.0 ? beta : alpha);
-            }
+            const double tau = s_sc[0], scale = s_sc[2];
             if (mine && !piv && pos == s) pos = s_ppos;  // the column at position s takes the pivot's place
             if (piv) pos = s;
-            __syncthreads();
             // ---- trailing update + downdate (qr.cpp:93-106), step-specialised ----
-            if (mine) {
-                if (piv) {
-                    switch (s) {
-#define IDK_PIV_CASE(r) \
-    case r:             \
-        if constexpr (r < M) pivot_step<M, (r < M ? r : 0)>(y, vfull, tau, beta); \
-        break;
-                        IDK_REP32(IDK_PIV_CASE)
-#undef IDK_PIV_CASE
-                        default:
-                            break;
-                    }
-                } else if (pos > s) {
+            if (mine && !piv && pos > s) {
+                {
                     switch (s) {
 #define IDK_COL_CASE(r) \
     case r:             \
-        if constexpr (r < M) column_step<M, (r < M ? r : 0)>(y, vfull, tau, live, anchor, pa, pt); \
+        if constexpr (r < M) column_step<M, (r < M ? r : 0)>(y, colbuf, tau, scale, live, anchor, pa, pt); \
         break;
                         IDK_REP32(IDK_COL_CASE)
 #undef IDK_COL_CASE
