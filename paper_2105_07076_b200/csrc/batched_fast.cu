@@ -228,11 +228,9 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
             const unsigned best = __reduce_min_sync(0xffffffffu, lane < kFastThreads / 32 ? red_u[lane] : 0xffffffffu);
             const bool piv = mine && static_cast<unsigned>(pos) == best;
             if (piv) {  // publish the pivot column and its reflector (qr.cpp:16-28)
+                double2* cb2 = reinterpret_cast<double2*>(colbuf);  // 16-byte aligned: LDS, M even
 #pragma unroll
-                for (int i = 0; i < M; ++i) colbuf[i] = y[i];
-#pragma unroll
-                for (int i = 0; i < KM; ++i)  // R(0..s-1, s) of this column
-                    if (i < s) r11[s * KM + i] = y[i];
+                for (int i = 0; i < M; i += 2) cb2[i >> 1] = make_double2(y[i], y[i + 1]);
                 const int len = m - s;
                 double tau = 0.0, beta = pa, scale = 1.0;
                 if (len > 1 && pt != 0.0) {
@@ -251,6 +249,7 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
             const double tau = s_sc[0], scale = s_sc[2];
             if (mine && !piv && pos == s) pos = s_ppos;  // the column at position s takes the pivot's place
             if (piv) pos = s;
+            if (c < s) r11[s * KM + c] = colbuf[c];  // R(0..s-1, s), copied in parallel
             // ---- trailing update + downdate (qr.cpp:93-106), step-specialised ----
             if (mine && !piv && pos > s) {
                 {
