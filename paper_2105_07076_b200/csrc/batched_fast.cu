@@ -88,6 +88,20 @@ __device__ __forceinline__ double lds_v(const double* p) {
     return v;
 }
 
+// The reflector this column would produce as the next pivot (qr.cpp:16-28),
+// formed by every live column in the parallel phase so the elected pivot
+// only publishes it.
+__device__ __forceinline__ void reflector(double pa, double pt, int len, double& tau, double& beta, double& scale) {
+    tau = 0.0;
+    beta = pa;
+    scale = 1.0;
+    if (len > 1 && pt != 0.0) {
+        beta = -copysign(sqrt(add_rn(mul_rn(pa, pa), pt)), pa);
+        tau = (beta - pa) / beta;
+        scale = 1.0 / (pa - beta);
+    }
+}
+
 // Trailing update of one non-pivot column at compile-time step S: dot with
 // v = [1; scale * p] (p = the pivot column below row S), axpy, downdate,
 // recompute, next-step partials -- every loop
@@ -96,7 +110,8 @@ __device__ __forceinline__ double lds_v(const double* p) {
 // column is not spilled.
 template <int M, int S>
 __device__ __forceinline__ void column_step(double (&y)[M], const double* __restrict__ pcol, double tau,
-                                            double scale, double& live, double& anchor, double& pa, double& pt) {
+                                            double scale, double& live, double& anchor, double& pa, double& pt,
+                                            int m, double& rt, double& rb, double& rs) {
     const double ys = y[S];
     double head = ys;
     if (tau != 0.0) {
@@ -147,6 +162,7 @@ __device__ __forceinline__ void column_step(double (&y)[M], const double* __rest
         anchor = lv;
     }
     live = lv;
+    reflector(pa, pt, m - (S + 1), rt, rb, rs);
 }
 
 #define IDK_REP32(M) \
@@ -212,6 +228,8 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
             pt = s0 + s1;
             live = anchor = fma(y[0], y[0], pt);
         }
+        double rt, rb, rs;
+        reflector(pa, pt, m, rt, rb, rs);
         int pos = c;
 
         for (int s = 0; s < k; ++s) {
@@ -231,13 +249,7 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
                 double2* cb2 = reinterpret_cast<double2*>(colbuf);  // 16-byte aligned: LDS, M even
 #pragma unroll
                 for (int i = 0; i < M; i += 2) cb2[i >> 1] = make_double2(y[i], y[i + 1]);
-                const int len = m - s;
-                double tau = 0.0, beta = pa, scale = 1.0;
-                if (len > 1 && pt != 0.0) {
-                    beta = -copysign(sqrt(add_rn(mul_rn(pa, pa), pt)), pa);
-                    tau = (beta - pa) / beta;
-                    scale = 1.0 / (pa - beta);
-                }
+                const double tau = rt, beta = rb, scale = rs;
                 s_sc[0] = tau;
                 s_sc[1] = beta;
                 s_sc[2] = scale;
@@ -256,7 +268,7 @@ batched_fast_kernel(const double* __restrict__ A, int64_t lda, int64_t stride, i
                     switch (s) {
 #define IDK_COL_CASE(r) \
     case r:             \
-        if constexpr (r < M) column_step<M, (r < M ? r : 0)>(y, colbuf, tau, scale, live, anchor, pa, pt); \
+        if constexpr (r < M) column_step<M, (r < M ? r : 0)>(y, colbuf, tau, scale, live, anchor, pa, pt, m, rt, rb, rs); \
         break;
                         IDK_REP32(IDK_COL_CASE)
 #undef IDK_COL_CASE
