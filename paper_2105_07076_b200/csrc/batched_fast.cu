@@ -71,10 +71,14 @@ __device__ __forceinline__ double wmax_nonneg(double v) {
     return r == 0ull ? -1.0 : __longlong_as_double(static_cast<long long>(r - 1ull));
 }
 
+// The two square roots of the tie band are cold code: out of line, so the
+// step loop's serial phase does not carry them.
+__device__ __noinline__ bool tie_band(double v, double vmax) { return sqrt(v) >= (1.0 - 1e-14) * sqrt(vmax); }
+
 __device__ __forceinline__ bool tie_ok(double v, double vmax) {  // qr.cpp:71-73, exact
     if (v == vmax) return true;
     if (!(v >= vmax * (1.0 - 4e-14))) return false;
-    return sqrt(v) >= (1.0 - 1e-14) * sqrt(vmax);
+    return tie_band(v, vmax);
 }
 
 }  // namespace
