@@ -1,21 +1,21 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the B200 ID path on BASELINE.json's workload.
 
-Default workload (N=1): BASELINE configs[1] ("cfg2"): Gaussian-sketch RID of a
-2000 x 4000 fp64 A = U diag(exp(-i/30)) V^T, k = 100, p = 10, Omega from the
-on-device Philox generator.  A "step" is 64 distinct cfg2 IDs (sketch -> CPQR
--> Z -> C each) in flight at once through the C ABI's concurrent entry
-(idk_id_auto_batch: one stream per ID), inputs already resident in HBM
-(`--batch 1`: one ID per step through idk_id_auto).  L2 (126 MB) is flushed
-with a 256 MiB memset between timed steps (the 64 inputs are 4 GB); only the
-step itself is inside the CUDA events.
+Default workload (N=1): the largest single-GPU configuration, BASELINE
+configs[3] ("cfg4"): Gaussian-sketch RID of a 16384 x 16384 fp64
+A = U diag(sigma) V^T (sigma_i = 1 for i < 128, (i-127)^-2 after), k = 256,
+p = 16, Omega from the on-device Philox generator.  A "step" is one full ID
+(Omega -> sketch Y = Omega A -> CPQR(Y) -> Z -> C) through the C ABI
+(idk_id_auto), input resident in HBM; A (2 GiB) is larger than L2 and L2 is
+also flushed with a 256 MiB memset between timed steps (outside the events).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1..cfg5]
   python bench.py --impl reference ...   # the reference's CPU path (oracle/_ref)
 
-N > 1 is launched by torchrun, one rank per GPU; cfg1/cfg2 run as independent
-replicas ("replicas only"), cfg3 partitions the batch by matrix.
-Rank 0 prints one JSON line.
+--gpus N > 1 without a launcher re-executes itself under torch.distributed.run
+(one rank per GPU, NCCL).  cfg4/cfg5 are column-sharded;
+cfg3 partitions the batch by matrix; cfg1/cfg2 run as independent replicas
+("replicas only").  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -44,11 +44,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--seed", type=int, default=20260601)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0,
+                    help="cfg1-3: time budget of the 1-thread cpu_baseline repeats (cfg4/cfg5: one full run)")
     ap.add_argument("--shard", action="store_true", help="cfg4/cfg5: use the sharded layer even at N=1")
     ap.add_argument("--batch", type=int, default=None,
                     help="cfg1/cfg2: distinct matrices per step, run concurrently through idk_id_auto_batch "
@@ -171,26 +172,44 @@ def stage_rooflines(cfg, stage_avg, peaks, fp64_peak):
             gb = w["bytes"] / (ms / 1e3) / 1e9
             out[st] = {"bound": "hbm" if st != "cpqr" else "latency (k dependent steps)", "achieved": gb,
                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gb / peaks["hbm_gbs"], "avg_launch_ms": ms}
+            if st == "cpqr":
+                out[st]["per_pivot_step_us"] = 1e3 * ms / cfg.k
+        out[st]["kernel"] = stage_kernels(cfg).get(st, st)
     return out
 
 
-def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic, dual=False):
+def stage_kernels(cfg):
+    """The kernels each stage launches for this config (what actually runs)."""
+    tall = cfg.m > cfg.n
+    k = cfg.k
+    if k <= 128:
+        trsm = f"id_trsm_dmma_kernel<{(k + 31) // 32}>"
+    elif k <= 256:
+        trsm = f"id_trsm_dmma_big_kernel<{(k + 31) // 32}>"
+    else:
+        trsm = "id_trsm_rl_kernel"
+    return {
+        "prep": "omega_philox_kernel" if cfg.randomized else ("transpose_kernel" if tall else "cudaMemcpy2DAsync"),
+        "sketch": f"sketch_tma_kernel<WM, {'true' if tall else 'false'}> + splitk_reduce_kernel (TMA-fed DMMA m8n8k4)",
+        "cpqr": "cpqr_resident_kernel (on-chip CPQR; 16-CTA cluster DSMEM exchange or one CTA per SM grid exchange)",
+        "solve": "gather_r11_kernel + " + trsm,
+        "gather": "gather_rows_kernel" if tall else "gather_columns_vec_kernel",
+        "batched": "batched_fast_kernel<64, 16>",
+    }
+
+
+def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic, cfg):
     secs = avg_ms / 1e3
-    if stage == "sketch":
+    kern = stage_kernels(cfg).get(stage, stage)
+    if stage in ("sketch", "solve") and "flops" in work:
         achieved = work["flops"] / secs / 1e12
-        kern = ("sketch_tma_kernel<WM, true> (TMA-fed DMMA m8n8k4, A read transposed)" if dual
-                else "sketch_tma_kernel<WM, false> (TMA-fed DMMA m8n8k4)")
         return {"kernel": kern, "bound": "tensor", "achieved": achieved,
                 "peak": fp64_peak["tflops"], "unit": "TFLOP/s", "frac": achieved / fp64_peak["tflops"],
                 "peak_source": fp64_peak["source"], "traffic": traffic, "avg_launch_ms": avg_ms,
                 "algorithmic_per_launch": work["flops"]}
     achieved = work["bytes"] / secs / 1e9
-    names = {"cpqr": "cpqr_resident_kernel (on-chip CPQR, cluster DSMEM / grid exchange)",
-             "solve": "gather_r11_kernel + id_trsm_warp_kernel",
-             "gather": "gather_columns_kernel", "prep": "omega_philox_kernel / working copy",
-             "batched": "batched_id_kernel"}
-    return {"kernel": names.get(stage, stage), "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+    return {"kernel": kern, "bound": "latency" if stage == "cpqr" else "hbm", "achieved": achieved,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)", "traffic": traffic, "avg_launch_ms": avg_ms,
             "algorithmic_per_launch": work["bytes"]}
 
@@ -237,6 +256,9 @@ def run_ours(args):
         a = a[b3:e3].contiguous()
     elif use_sharded:                              # this rank's block, stored contiguously
         a = (a[begin:end, :] if tall else a[:, begin:end]).t().contiguous().t()
+    nccl_path = use_sharded and backend == "nccl"  # the C-ABI entry idk_id_sharded over its own NCCL communicator
+    if nccl_path:
+        sharded.nccl_setup(local)
     torch.cuda.empty_cache()
     ctx = idk.context(local)
     ctx.set_profiling(False)  # per-stage events cost ~35% with 8 IDs in flight: a separate pass records them
@@ -256,6 +278,8 @@ def run_ours(args):
             return idk.id_auto_batch(mats, k, method, seeds=bseeds, p=p, out=bout, lanes=nb)
         if cfg.name == "cfg3":
             return idk.optim_id_batched(a, k)
+        if nccl_path:
+            return sharded.id_sharded_nccl(a, n_dec, k, p, seed=args.seed, transposed=tall)
         if use_sharded:
             return sharded.sketch_rid_sharded(a, n_dec, k, p, seed=args.seed, transposed=tall)
         if cfg.randomized:
@@ -376,7 +400,10 @@ def run_ours(args):
             if use_sharded:  # this rank's shard in from pinned memory, its Z block and C out
                 da = torch.empty_like(a)
                 da.copy_(pinned.t(), non_blocking=True)
-                cols, zl, c = sharded.sketch_rid_sharded(da, n_dec, k, p, seed=args.seed, transposed=tall)
+                if nccl_path:
+                    cols, zl, c = sharded.id_sharded_nccl(da, n_dec, k, p, seed=args.seed, transposed=tall)
+                else:
+                    cols, zl, c = sharded.sketch_rid_sharded(da, n_dec, k, p, seed=args.seed, transposed=tall)
                 cols.cpu(), zl.cpu(), c.cpu()
                 return
             idk.id_auto(ha, k, method, seed=args.seed, p=p)
@@ -415,7 +442,8 @@ def run_ours(args):
         e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "h2d_gbs": e2e_val / max(ids / ke, 1) * h2d / 1e9,
                "h2d_peak_gbs": 55.1, "h2d_peak_source": "profiles/probe_h2d_r01.txt (pinned H2D, measured)",
-               "api": ("paper_2105_07076_b200.sharded.sketch_rid_sharded (per-rank shard, pinned host)" if use_sharded
+               "api": ("idk_id_sharded via sharded.id_sharded_nccl (per-rank shard from pinned host)" if nccl_path else
+                       "paper_2105_07076_b200.sharded.sketch_rid_sharded (per-rank shard, pinned host)" if use_sharded
                        else "idk_id_auto_host_many (include/idkit_b200.h): pinned host buffers, upload/compute/"
                             "download overlapped across steps")}
 
@@ -430,8 +458,7 @@ def run_ours(args):
         stage_avg = {s_: v / n_stage for s_, v in stage_tot.items()}
         dom = max(stage_avg, key=stage_avg.get)
         traffic = (ncu.get(cfg.name) or {}).get(dom, {}).get("dram_bytes_per_launch")
-        roofline = roofline_for(dom, stage_work(cfg, cfg.n)[dom], stage_avg[dom], peaks, fp64, traffic,
-                                dual=cfg.m > cfg.n)
+        roofline = roofline_for(dom, stage_work(cfg, cfg.n)[dom], stage_avg[dom], peaks, fp64, traffic, cfg)
         # share of the device time per ID (with nb IDs in flight, per-launch times include co-running kernels)
         roofline["step_share"] = stage_avg[dom] / sum(stage_avg.values())
         if dom == "cpqr":  # k dependent pivot steps: latency-bound, report the per-step time
@@ -448,7 +475,7 @@ def run_ours(args):
         per = a.shape[0]
         bytes_ = 8.0 * per * (cfg.m * cfg.n + cfg.k * cfg.n + cfg.m * cfg.k) + 8.0 * per * cfg.k
         traffic = (ncu.get(cfg.name) or {}).get("batched", {}).get("dram_bytes_per_launch")
-        roofline = roofline_for("batched", {"bytes": bytes_}, total_ms / args.steps, peaks, fp64, traffic)
+        roofline = roofline_for("batched", {"bytes": bytes_}, total_ms / args.steps, peaks, fp64, traffic, cfg)
     if peaks.get("_fallback") and roofline:
         roofline["peak_source"] = "fallback 6.65 TB/s (B200_PROFILING.md)"
 
@@ -458,8 +485,14 @@ def run_ours(args):
         cpu = cpu_baseline(cfg, a, args)
 
     if rank == 0:
-        par = ("replicas" if replicas else ("partition-by-matrix" if cfg.name == "cfg3" else
-                                            "column-sharded sketch + all_gather(Y)")) + f" x{world}"
+        if replicas:
+            par = f"replicas x{world}"
+        elif cfg.name == "cfg3":
+            par = f"partition-by-matrix x{world}" if world > 1 else "single GPU (whole batch)"
+        elif use_sharded:
+            par = f"column-sharded x{world}: local sketch, all_gather_into_tensor(Y), replicated CPQR, local Z"
+        else:
+            par = "single GPU (no sharding)"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -470,6 +503,7 @@ def run_ours(args):
                        "ids_in_flight": nb if replicas else None,
                        "api": ("idk_id_auto_batch (one lane stream per ID in flight)" if nb > 1 else
                                "idk_optim_id_batched" if cfg.name == "cfg3" else
+                               "idk_id_sharded (NCCL inside the C ABI)" if nccl_path else
                                "sharded.sketch_rid_sharded" if use_sharded else "idk_id_auto"),
                        "parallelism": par,
                        "l2": "flushed between timed steps (256 MiB memset, outside the events)",
@@ -487,6 +521,21 @@ def run_ours(args):
 # ---------------------------------------------------------------------------------
 # reference CPU path (oracle/_ref = the reference sources compiled in place)
 # ---------------------------------------------------------------------------------
+def host_info():
+    """nproc and CPU model of this host (BASELINE.md section 2 asks for both)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    return {"nproc": threads, "cpu_model": model}
+
+
 def _ref_lib():
     from oracle import Oracle, Reference
     if Reference.available():
@@ -494,157 +543,204 @@ def _ref_lib():
     return Oracle(), "port"
 
 
-def _ref_call(lib, kind, cfg, a, omega):
-    if cfg.name == "cfg3":
-        for b in range(a.shape[0]):
-            ab = a[b].T
-            if kind == "reference":
-                lib.sketch_id(ab, cfg.k, None, want_c=True)
-            else:
-                lib.interp_decomp(ab, cfg.k)
-        return
-    if kind == "reference":
-        lib.sketch_id(a, cfg.k, omega, want_c=True)
-    else:
-        lib.interp_decomp(a, cfg.k, omega)
-
-
-def _ref_inputs(cfg, a_dev=None, seed=20260601, cfg3_sample=64):
+def _ref_inputs(cfg, seed, a_dev=None):
+    """Host inputs of the workload.  cfg4/cfg5 (2 GiB) are built on the GPU when
+    one is present (harness construction only, make_torch) and copied to the
+    host; otherwise numpy builds them (slow)."""
     import numpy as np
-    from oracle import Oracle
-    from paper_2105_07076_b200.configs import make_np
-    if cfg.name == "cfg3":
-        a = make_np("cfg3", seed=seed, scale=cfg3_sample / cfg.batch)
-        return a, None
+    from paper_2105_07076_b200.configs import make_np, make_torch
     if a_dev is not None:
-        a = a_dev.cpu().numpy()
-        a = np.asfortranarray(a)
-    else:
-        a = make_np(cfg.name, seed=seed)
-    if cfg.m > cfg.n:
-        a = np.asfortranarray(a.T)  # the dual runs on A^T (id.cpp:85)
-    omega = Oracle().omega_philox(cfg.l, a.shape[0], seed) if cfg.randomized else None
-    return a, omega
-
-
-def _timed_parallel(lib, kind, cfg, a, omega, threads):
-    errs = []
-
-    def work():
+        return a_dev.cpu().numpy() if cfg.name == "cfg3" else np.asfortranarray(a_dev.cpu().numpy())
+    if cfg.name in ("cfg4", "cfg5"):
         try:
-            _ref_call(lib, kind, cfg, a, omega)
-        except Exception as e:  # noqa: BLE001
-            errs.append(e)
+            import torch
+            if torch.cuda.is_available():
+                t = make_torch(cfg.name, seed=seed)
+                out = np.asfortranarray(t.cpu().numpy())
+                del t
+                torch.cuda.empty_cache()
+                return out
+        except Exception:  # noqa: BLE001 -- fall back to the host construction
+            pass
+    return make_np(cfg.name, seed=seed)
 
-    ts = [threading.Thread(target=work) for _ in range(threads)]
-    t0 = time.perf_counter()
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    dt = time.perf_counter() - t0
-    if errs:
-        raise errs[0]
-    return dt
+
+class RefPath:
+    """The reference's CPU implementation of the path on `threads` host threads.
+
+    cfg1 / cfg3: idkit::optim_id (id.cpp:29-45; cfg3: the 4096 independent calls
+    spread over the threads).  cfg2 / cfg4 / cfg5: the composed
+    sketch path generate(gaussian) -> matmul -> qr_column_pivoted ->
+    solve_triangular -> select_columns (the reference has no sketch RID; SURVEY.md
+    section 8(c)); with several threads matmul and solve_triangular are split by
+    column blocks, which is bit-identical to the single call (ref_sketch_id_mt).
+    cfg1 / cfg2 are too small to split: one ID per thread, `threads` IDs per step.
+    """
+
+    def __init__(self, cfg, a, threads, seed):
+        self.cfg, self.a, self.threads, self.seed = cfg, a, threads, seed
+        self.lib, self.kind = _ref_lib()
+        self.stage_s = None
+
+    @property
+    def ids_per_call(self):
+        if self.cfg.name == "cfg3":
+            return self.a.shape[0]
+        return self.threads if self.cfg.name in ("cfg1", "cfg2") else 1
+
+    def _one(self):
+        cfg, a = self.cfg, self.a
+        if cfg.name == "cfg1":
+            if self.kind == "reference":
+                self.lib.optim_id(a, cfg.k)
+            else:
+                self.lib.optim_id(a, cfg.k, want_approx=True)
+        elif self.kind == "reference":
+            _, _, _, self.stage_s = self.lib.sketch_id_mt(a, cfg.k, None, l=cfg.l, seed=self.seed,
+                                                          transposed=cfg.m > cfg.n, threads=1)
+        else:
+            om = self.lib.generate(1, cfg.l, a.shape[1] if cfg.m > cfg.n else a.shape[0], self.seed)
+            self.lib.interp_decomp(np.asfortranarray(a.T) if cfg.m > cfg.n else a, cfg.k, om)
+
+    def call(self):
+        """One step; returns wall seconds."""
+        cfg = self.cfg
+        t0 = time.perf_counter()
+        if cfg.name == "cfg3":
+            if self.kind == "reference":
+                self.lib.optim_id_batch_mt(self.a, cfg.k, threads=self.threads)
+            else:
+                for b in range(self.a.shape[0]):
+                    self.lib.optim_id(np.asfortranarray(self.a[b].T), cfg.k, want_approx=True)
+        elif cfg.name in ("cfg1", "cfg2"):
+            errs = []
+
+            def work():
+                try:
+                    self._one()
+                except Exception as e:  # noqa: BLE001
+                    errs.append(e)
+            ts = [threading.Thread(target=work) for _ in range(self.threads)]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            if errs:
+                raise errs[0]
+        elif self.kind == "reference":
+            _, _, _, self.stage_s = self.lib.sketch_id_mt(self.a, cfg.k, None, l=cfg.l, seed=self.seed,
+                                                          transposed=cfg.m > cfg.n, threads=self.threads)
+        else:
+            self._one()
+        return time.perf_counter() - t0
+
+    def describe(self):
+        cfg = self.cfg
+        if cfg.name == "cfg3":
+            what = f"the full batch of {self.a.shape[0]} {cfg.m}x{cfg.n} matrices through optim_id"
+        elif cfg.name == "cfg1":
+            what = f"{self.threads} concurrent optim_id calls (one per thread) on {cfg.m}x{cfg.n}"
+        elif cfg.name == "cfg2":
+            what = (f"{self.threads} concurrent composed sketch IDs (one per thread): generate(gaussian) -> "
+                    "matmul -> qr_column_pivoted -> solve_triangular -> select_columns")
+        else:
+            what = ("one full composed sketch ID: generate(gaussian) -> " +
+                    ("transpose(A rows) -> " if cfg.m > cfg.n else "") +
+                    "matmul -> qr_column_pivoted -> solve_triangular -> select_columns"
+                    + (", matmul / solve_triangular split by column blocks over the threads (bit-identical)"
+                       if self.threads > 1 else ""))
+        return what
+
+
+import numpy as np  # noqa: E402  (used by RefPath; bench's GPU arm imports lazily)
 
 
 def cpu_baseline(cfg, a_dev, args):
-    """The reference's CPU path on this host: bounded sample, 1 thread (the reference is single-threaded)."""
-    if cfg.name in ("cfg4", "cfg5"):
-        return cpu_baseline_staged(cfg, a_dev, args)
-    lib, kind = _ref_lib()
-    a, omega = _ref_inputs(cfg, a_dev, seed=args.seed)
-    ids_each = a.shape[0] if cfg.name == "cfg3" else 1
-    dt1 = _timed_parallel(lib, kind, cfg, a, omega, 1)  # warm-up + estimate
-    reps = max(1, int(args.cpu_seconds / max(dt1, 1e-3)))
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        _ref_call(lib, kind, cfg, a, omega)
-    dt = time.perf_counter() - t0
-    return {"value": reps * ids_each / dt, "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": f"{reps} x {'batch of ' + str(ids_each) + ' IDs' if cfg.name == 'cfg3' else 'full ID'} "
-                      f"of {cfg.name} on 1 thread ({dt:.1f} s), composed reference path "
-                      "(matmul -> qr_column_pivoted -> solve_triangular -> select_columns)"}
-
-
-def cpu_baseline_staged(cfg, a_dev, args):
-    """cfg4/cfg5: one reference ID takes minutes, so the reference's stages are
-    timed separately on 1 thread -- matmul(Omega, M) on a column block of M,
-    scaled to all n columns, plus qr_column_pivoted(Y, k), solve_triangular and
-    the column gather at full size on the real Y (computed here by our sketch;
-    it equals the reference's matmul up to rounding)."""
-    import numpy as np
-    import paper_2105_07076_b200 as idk
-    lib, kind = _ref_lib()
-    tall = cfg.m > cfg.n
-    mm, nn = (cfg.n, cfg.m) if tall else (cfg.m, cfg.n)  # M = A^T (dual) or A: mm x nn
-    k = cfg.k
-    om = idk.sketch_omega(cfg.l, mm, args.seed)
-    y = np.asfortranarray(idk.sketch(om, a_dev, transposed=tall).cpu().numpy())
-    omh = np.asfortranarray(om.cpu().numpy())
-    nb = max(64, min(nn, int(nn * 0.03)))  # ~3% of the columns
-    blk = a_dev[:nb, :].t() if tall else a_dev[:, :nb]  # mm x nb block of M
-    blk = np.asfortranarray(blk.cpu().numpy())
-    t0 = time.perf_counter()
-    lib.matmul(omh, blk)
-    t_mm = (time.perf_counter() - t0) * nn / nb
-    t0 = time.perf_counter()
-    _, r, perm = lib.qr_column_pivoted(y, k)
-    t_qr = time.perf_counter() - t0
-    r = np.asfortranarray(r)
-    t0 = time.perf_counter()
-    lib.solve_triangular(np.asfortranarray(r[:, :k]), np.asfortranarray(r[:, k:]))
-    t_sv = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    a_h = blk  # the gather reads k columns (rows for the dual) of A: timed on the host copy of a block
-    np.asfortranarray(a_h[:, perm[:k] % a_h.shape[1]])
-    t_g = (time.perf_counter() - t0) * max(1.0, mm / a_h.shape[0])
-    total = t_mm + t_qr + t_sv + t_g
-    return {"value": 1.0 / total, "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": (f"staged estimate, 1 thread: reference matmul(Omega, M) on {nb} of {nn} columns "
-                       f"scaled x{nn / nb:.1f} ({t_mm:.1f} s), qr_column_pivoted({cfg.l}x{nn}, k={k}) "
-                       f"{t_qr:.1f} s, solve_triangular {t_sv:.1f} s, gather {t_g:.2f} s on the real Y "
-                       f"(Y from our sketch, equal to the reference's matmul up to rounding)")}
+    """The reference's CPU path on this host, 1 thread (the reference is
+    single-threaded), a full ID (cfg3: the full batch) -- no extrapolation."""
+    a = _ref_inputs(cfg, args.seed, a_dev)
+    rp = RefPath(cfg, a, 1, args.seed)
+    budget = args.cpu_seconds
+    dt = rp.call()  # cfg4 / cfg5: the one measured run (minutes on one core)
+    reps, total = 1, dt
+    if cfg.name not in ("cfg4", "cfg5"):  # warm-up done: time the median of up to 5 runs within the budget
+        times = []
+        while len(times) < 5 and (sum(times) < budget or len(times) < 1):
+            times.append(rp.call())
+        reps, total = len(times), statistics.median(times) * len(times)
+    out = {"value": reps * rp.ids_per_call / total, "unit": UNIT, "cores": 1, "kind": rp.kind,
+           "sample": f"{reps} x [{rp.describe()}] on 1 thread; " +
+                     (f"median of {reps} after a warm-up run" if reps > 1 else f"single run, {total:.1f} s"),
+           **host_info()}
+    if rp.stage_s:
+        out["stage_seconds"] = rp.stage_s
+    return out
 
 
 def run_reference(args):
     from paper_2105_07076_b200.configs import CONFIGS
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:  # the ranks meet once (gloo), then rank 0 alone runs the CPU reference
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        dist.barrier()
+        dist.destroy_process_group()
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
+    info = host_info()
+    threads = info["nproc"]
     base = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world, "higher_is_better": True,
-            "dtype": "f64", "config": {"workload": workload_desc(cfg), "m": cfg.m, "n": cfg.n, "k": cfg.k,
-                                       "p": cfg.p, "batch": cfg.batch}, "vs_baseline": None}
-    if cfg.name in ("cfg4", "cfg5"):
-        base.update({"unavailable": "one reference ID at this size takes minutes (cfg4 ~95 s on one core)"})
-        print(json.dumps(base), flush=True)
-        return
-    lib, kind = _ref_lib()
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    a, omega = _ref_inputs(cfg, None, seed=args.seed, cfg3_sample=64)
-    ids_each = (a.shape[0] if cfg.name == "cfg3" else 1) * threads
+            "scaling": "weak" if cfg.name in ("cfg1", "cfg2") else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded BASELINE construction (" + cfg.name + ")",
+            "config": {"workload": workload_desc(cfg), "m": cfg.m, "n": cfg.n, "k": cfg.k, "p": cfg.p,
+                       "batch": cfg.batch}}
+    a = _ref_inputs(cfg, args.seed)
+    rp = RefPath(cfg, a, threads, args.seed)
     t_w = 0.0
-    for _ in range(max(1, min(args.warmup, 1))):
-        t_w = _timed_parallel(lib, kind, cfg, a, omega, threads)
+    warm = max(0, min(args.warmup, 1))
+    for _ in range(warm):
+        t_w = rp.call()
     budget = 150.0
-    steps = max(1, min(args.steps, int(budget / max(t_w, 1e-3))))
-    total = 0.0
-    for _ in range(steps):
-        total += _timed_parallel(lib, kind, cfg, a, omega, threads)
-    value = steps * ids_each / total
-    sample = (f"each step: {threads} threads x one {cfg.name} ID each" if cfg.name != "cfg3" else
-              f"each step: {threads} threads x 64 of the 4096 {cfg.m}x{cfg.n} matrices") + \
-             f"; {steps} timed steps (requested {args.steps}, capped to ~{budget:.0f} s)"
-    base.update({"value": value, "steps": steps, "warmup": 1, "ms_per_step": 1e3 * total / steps,
-                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+    steps = args.steps if t_w <= 0 else max(1, min(args.steps, int(budget / t_w)))
+    times = [rp.call() for _ in range(steps)]
+    total = sum(times)
+    value = steps * rp.ids_per_call / total
+    sample = (f"each step: {rp.describe()}; {threads} threads; {steps} timed steps (requested {args.steps}, "
+              f"capped to ~{budget:.0f} s), {warm} warm-up")
+    base.update({"value": value, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * total / steps,
+                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": rp.kind, "sample": sample,
+                                  **info},
                  "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    if rp.stage_s:
+        base["stage_seconds_last_step"] = rp.stage_s
     print(json.dumps(base), flush=True)
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 without a launcher: re-exec this script under
+    torch.distributed.run, one rank per GPU (NCCL's INIT log stays on so the
+    communicator size can be checked)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; the launcher's world size wins", file=sys.stderr)
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: --warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3

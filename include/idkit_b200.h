@@ -49,7 +49,7 @@ typedef enum {
     IDK_ERR_NOT_POSDEF = 3,   /* idkit::NotPositiveDefiniteError (solve.cpp:66-68)         */
     IDK_ERR_CUDA = 4,         /* CUDA runtime failure / no sm_100 device                   */
     IDK_ERR_NO_MEMORY = 5,    /* device allocation failed                                  */
-    IDK_ERR_NCCL = 6          /* reserved for the sharded host layer                       */
+    IDK_ERR_NCCL = 6          /* NCCL missing or a collective failed (idk_id_sharded)     */
 } idk_status;
 
 /* How the Gaussian sketch Omega (l x m) is produced. */
@@ -69,6 +69,14 @@ typedef enum {
                                     of AUTO's cluster push exchange; selectable for testing)                 */
 } idk_cpqr_mode;
 
+/* Arithmetic of the sketch Y = Omega M. */
+typedef enum {
+    IDK_SKETCH_DMMA = 0,            /* default: FP64 tensor cores (DMMA), fixed-order split-K; deterministic */
+    IDK_SKETCH_REFERENCE_ORDER = 1  /* the reference matmul's arithmetic (matrix.cpp:28-48: sequential sum,
+                                       unfused multiply and add): Y bit-identical to idkit::matmul(Omega, M);
+                                       SIMT, an order of magnitude slower -- for bit-compatibility checks   */
+} idk_sketch_order;
+
 /* ---- handle ---------------------------------------------------------------- */
 IDK_API int idk_abi_version(void);
 IDK_API int idk_create(idk_handle* out, int device);
@@ -81,6 +89,8 @@ IDK_API const char* idk_status_string(int status);
 IDK_API int64_t idk_kernel_launches(idk_handle h);
 /* Select the CPQR kernel (idk_cpqr_mode); default IDK_CPQR_AUTO. */
 IDK_API int idk_set_cpqr_mode(idk_handle h, int mode);
+/* Select the sketch arithmetic (idk_sketch_order) of idk_sketch_rid / idk_id_auto; default DMMA. */
+IDK_API int idk_set_sketch_order(idk_handle h, int order);
 /* Batched entry: 1 = the bit-identical kernel (reference summation order,
  * unfused IEEE ops); 0 (default) = the throughput kernel (registers + TMA
  * prefetch + FMA), which matches within rounding. */
@@ -176,6 +186,47 @@ IDK_API int idk_optim_id_batched_host(idk_handle h, const double* h_a, int64_t b
  * host layer (paper_2105_07076_b200/sharded.py, torch.distributed/NCCL). */
 IDK_API int idk_id_from_sketch(idk_handle h, double* d_y, int64_t l, int64_t n, int64_t ldy, int64_t k,
                                int64_t c_begin, int64_t c_end, int64_t* d_cols, double* d_z_local);
+
+/* ---- multi-GPU: one process per GPU, column-sharded --
+ * The reference has no distributed layer; its sharded operation is matmul
+ * (matrix.cpp:28-48), whose output columns follow the input's.  These entries
+ * shard the decomposed matrix M by column blocks over the ranks of an NCCL
+ * communicator.  NCCL is bound at run time (the process's libnccl.so.2, e.g.
+ * torch's); the library does not link it. */
+
+/* Columns [*begin, *end) of an n-column M owned by `rank` of `nranks`: blocks
+ * of w = ceil(n / nranks) columns, rank r owning [min(r w, n), min((r+1) w, n)),
+ * so rank r's sketch block sits at column r*w of Y and a single in-place
+ * ncclAllGather assembles Y. */
+IDK_API int idk_shard_range(int64_t n, int nranks, int rank, int64_t* begin, int64_t* end);
+/* NCCL bootstrap: rank 0 calls idk_nccl_unique_id (128 bytes, ncclUniqueId) and
+ * distributes it through the caller's own channel; every rank then calls
+ * idk_comm_init on its handle (device = the handle's).  idk_set_nccl_comm
+ * attaches a caller-owned ncclComm_t instead (never destroyed here). */
+IDK_API int idk_nccl_unique_id(void* out128);
+IDK_API int idk_comm_init(idk_handle h, int nranks, int rank, const void* id128);
+IDK_API int idk_set_nccl_comm(idk_handle h, void* nccl_comm);
+IDK_API int idk_comm_destroy(idk_handle h);
+
+/* Sharded Gaussian-sketch RID (the north-star path over nranks GPUs; cfg4 /
+ * cfg5).  Every rank passes its block of M's columns [begin, end) from
+ * idk_shard_range: d_a_local is m x (end-begin) (lda >= m), or with
+ * a_transposed != 0 the same columns of M = A^T as the stored row block of the
+ * tall A, (end-begin) x m (lda >= end-begin) -- the id_auto dual (id.cpp:78-95).
+ * Per rank: Omega (identical everywhere: Philox keyed by seed, the reference's
+ * mt19937 stream, or verbatim) -> local DMMA sketch written into its slot of
+ * Y -> one in-place ncclAllGather of Y ((k+p) x n) -> the deterministic CPQR
+ * of Y, replicated (bit-identical on every rank, so no pivot broadcast) ->
+ * Z for the local columns into d_z_local (k x (end-begin), ld = k) -> the
+ * pivot columns this rank owns gathered into d_c and one grouped
+ * ncclBroadcast per column from its owner, so C (m x k, ld = m) is complete
+ * and bit-exact on every rank (optional).  d_cols (k) = global column ids of
+ * M (row ids of A for the dual).  Results equal idk_sketch_rid's on the
+ * unsharded matrix bit for bit.  Without a communicator the call runs as one
+ * rank. */
+IDK_API int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, int64_t lda, int a_transposed,
+                           int64_t k, int64_t p, uint64_t seed, int omega_mode, const double* d_omega,
+                           int64_t* d_cols, double* d_z_local, double* d_c);
 
 /* Concurrent entry for a stream of independent IDs (serving): `count` m x n
  * matrices d_a[i] (device, lda), results into d_cols[i], d_z[i] (k * max(m, n))

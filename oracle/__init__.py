@@ -333,6 +333,43 @@ class Reference(_Lib):
                                            C.c_int64(l), _ptr(cols), _ptr(z), _ptr(c)))
         return cols, z, c
 
+    def sketch_id_mt(self, a, k, omega=None, l=None, seed=0, transposed=False, threads=None, want_c=True):
+        """sketch_id on `threads` host threads (bit-identical to one thread: see
+        ref_sketch_id_mt).  `a` is the stored matrix (column-major, any ld);
+        transposed=True decomposes M = a^T (id_auto's dual).  omega=None ->
+        the reference's generate(gaussian, l, m, seed) inside the timed region.
+        Returns (cols, z, c, times) with times = {omega, matmul, qr, solve, select} s."""
+        if not (a.flags["F_CONTIGUOUS"] and a.dtype == np.float64):
+            a = _f64(a)
+        lda = a.shape[0]
+        m, n = (a.shape[1], a.shape[0]) if transposed else a.shape
+        om = _f64(omega) if omega is not None else None
+        ll = om.shape[0] if om is not None else int(l)
+        threads = threads or (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+        cols = np.empty(k, dtype=np.int64)
+        z = np.empty((k, n), order="F")
+        c = np.empty((m, k), order="F") if want_c else None
+        t5 = np.zeros(5)
+        self._check(self.lib.ref_sketch_id_mt(_ptr(a), C.c_int64(lda), C.c_int64(m), C.c_int64(n),
+                                              C.c_int(1 if transposed else 0), C.c_int64(k), _ptr(om),
+                                              C.c_int64(ll), C.c_uint64(seed), C.c_int(int(threads)), _ptr(cols),
+                                              _ptr(z), _ptr(c), _ptr(t5)))
+        names = ("omega", "matmul", "qr", "solve", "select")
+        return cols, z, c, dict(zip(names, t5.tolist()))
+
+    def optim_id_batch_mt(self, a, k, threads=None, want_approx=False):
+        """optim_id over a (batch, n, m) stack (matrix b column-major = a[b].T) on threads."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        batch, n, m = a.shape
+        threads = threads or (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+        cols = np.empty((batch, k), dtype=np.int64)
+        z = np.empty((batch, n, k))  # z[b] = Z_b^T storage: Z_b (k x n) column-major
+        approx = np.empty_like(a) if want_approx else None
+        self._check(self.lib.ref_optim_id_batch_mt(_ptr(a), C.c_int64(batch), C.c_int64(m), C.c_int64(n),
+                                                   C.c_int64(k), C.c_int(int(threads)), _ptr(cols), _ptr(z),
+                                                   _ptr(approx)))
+        return cols, z, approx
+
     def gram_schmidt_pivoted(self, a, steps):
         a = _f64(a)
         order = np.empty(steps, dtype=np.int64)

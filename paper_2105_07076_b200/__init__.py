@@ -8,12 +8,12 @@ reference's C++ API; `sharded` is the multi-GPU (torch.distributed) layer.
 """
 from .idkit import (DETERMINISTIC, OMEGA_MT19937, OMEGA_PHILOX, OMEGA_VERBATIM, RANDOMIZED, SAMPLED, Context, CudaError,
                     IdkitError, IdResult, InvalidArgument, NotPositiveDefiniteError, PivotedQr, SingularMatrixError,
-                    approx, context, diagnostics, matmul_ref, id_auto, id_auto_batch, id_auto_many, id_from_sketch, optim_id, optim_id_batched, optim_rid, qr_column_pivoted, select_columns, sketch,
+                    approx, context, diagnostics, id_sharded, nccl_unique_id, shard_range, matmul_ref, id_auto, id_auto_batch, id_auto_many, id_from_sketch, optim_id, optim_id_batched, optim_rid, qr_column_pivoted, select_columns, sketch,
                     sketch_omega, sketch_rid)
 
 __all__ = [
     "DETERMINISTIC", "RANDOMIZED", "SAMPLED", "OMEGA_PHILOX", "OMEGA_MT19937", "OMEGA_VERBATIM", "Context", "CudaError",
     "IdkitError", "IdResult", "InvalidArgument", "NotPositiveDefiniteError", "PivotedQr", "SingularMatrixError",
-    "approx", "context", "diagnostics", "matmul_ref", "id_auto", "id_auto_batch", "id_auto_many", "id_from_sketch", "optim_id", "optim_id_batched", "optim_rid", "qr_column_pivoted", "select_columns", "sketch",
+    "approx", "context", "diagnostics", "id_sharded", "nccl_unique_id", "shard_range", "matmul_ref", "id_auto", "id_auto_batch", "id_auto_many", "id_from_sketch", "optim_id", "optim_id_batched", "optim_rid", "qr_column_pivoted", "select_columns", "sketch",
     "sketch_omega", "sketch_rid",
 ]

@@ -25,6 +25,7 @@ SIGNATURES = {
     "idk_set_profiling": (C.c_int, [_P, C.c_int]),
     "idk_set_cpqr_mode": (C.c_int, [_P, C.c_int]),
     "idk_set_batched_exact": (C.c_int, [_P, C.c_int]),
+    "idk_set_sketch_order": (C.c_int, [_P, C.c_int]),
     "idk_debug_cpqr_trace": (C.c_int, [_P, _P]),
     "idk_cpqr_plan": (C.c_int, [_P, _I64, _I64, _I64, C.POINTER(C.c_int64)]),
     "idk_stage_times": (C.c_int, [_P, C.POINTER(C.c_double), C.c_int]),
@@ -51,6 +52,12 @@ SIGNATURES = {
     "idk_diagnostics": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _P, _I64, _P, _P, C.POINTER(C.c_double)]),
     "idk_id_auto_host_many": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P,
                                         C.POINTER(C.c_int)]),
+    "idk_shard_range": (C.c_int, [_I64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "idk_nccl_unique_id": (C.c_int, [_P]),
+    "idk_comm_init": (C.c_int, [_P, C.c_int, C.c_int, _P]),
+    "idk_set_nccl_comm": (C.c_int, [_P, _P]),
+    "idk_comm_destroy": (C.c_int, [_P]),
+    "idk_id_sharded": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _I64, _I64, C.c_uint64, C.c_int, _P, _P, _P, _P]),
     "idk_id_auto_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P,
                                    C.POINTER(C.c_int)]),
 }

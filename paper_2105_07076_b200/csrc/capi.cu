@@ -18,6 +18,7 @@
 
 #include "../../include/idkit_b200.h"
 #include "kernels.h"
+#include "nccl_api.h"
 
 struct idk_context {
     int device = 0;
@@ -40,6 +41,7 @@ struct idk_context {
     int64_t launches = 0;
     int cpqr_mode = IDK_CPQR_AUTO;
     bool batched_exact = false;
+    int sketch_order = IDK_SKETCH_DMMA;
     // pipelined host entry: status words land here (pinned) instead of a sync per ID
     int* async_status = nullptr;
     int* batched_status = nullptr;  // idk_optim_id_batched_host: device status words of the current chunk
@@ -60,6 +62,10 @@ struct idk_context {
     bool profiling = false;
     cudaEvent_t ev[6] = {};
     float stage_ms[5] = {};
+    // multi-GPU: the NCCL communicator of idk_id_sharded (idk_comm_init / idk_set_nccl_comm)
+    idk::ncclComm_t nccl_comm = nullptr;
+    bool nccl_owned = false;
+    int nranks = 1, rank = 0;
 };
 
 namespace {
@@ -187,14 +193,15 @@ int check_cpqr_fits(idk_context* h, int64_t mrows, int64_t n, const CpqrChoice& 
 }
 
 cudaError_t run_cpqr(idk_context* h, const CpqrChoice& ch, double* W, int64_t mrows, int64_t n, int64_t k, char* base,
-                     const CpqrWs& w) {
+                     const CpqrWs& w, int64_t ldw = 0) {
+    if (ldw < mrows) ldw = mrows;
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     double* taus = reinterpret_cast<double*>(base + w.taus);
     if (ch.resident)
-        return idk::cpqr_resident_launch(ch.plan, W, mrows, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv,
+        return idk::cpqr_resident_launch(ch.plan, W, ldw, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv,
                                          taus, base + w.pub, reinterpret_cast<unsigned*>(base + w.barrier), h->stream);
-    return idk::cpqr_launch(W, mrows, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
+    return idk::cpqr_launch(W, ldw, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
                             reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream);
 }
 
@@ -321,9 +328,14 @@ int sketch_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t 
     }
     mark(h, 1);
     double* Y = reinterpret_cast<double*>(h->ws + yofs);
-    IDK_CUDA(idk::sketch_gemm(omega, l, d_a, lda, trans, Y, l, static_cast<int>(l), n, m, splits,
-                              splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr, h->stream));
-    h->launches += splits > 1 ? 2 : 1;
+    if (h->sketch_order == IDK_SKETCH_REFERENCE_ORDER) {  // matrix.cpp:28-48 arithmetic: Y bit-identical to matmul
+        IDK_CUDA(idk::matmul_ref_order(omega, l, d_a, lda, l, n, static_cast<int>(m), Y, l, h->stream, trans));
+        h->launches += 1;
+    } else {
+        IDK_CUDA(idk::sketch_gemm(omega, l, d_a, lda, trans, Y, l, static_cast<int>(l), n, m, splits,
+                                  splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr, h->stream));
+        h->launches += splits > 1 ? 2 : 1;
+    }
     return factor_and_solve(h, ch, Y, l, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, false);
 }
 
@@ -360,10 +372,13 @@ int sampled_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t
     if (lda < (trans ? n : m)) return set_err(h, IDK_ERR_INVALID_ARG, "optim_rid: lda too small");
     const int64_t p = std::min(k + extra, n);
     const CpqrChoice ch = choose_cpqr(h, m, p, k);
-    if ((rc = check_cpqr_fits(h, m, p, ch))) return rc;
     // Tall samples: pivoted QR of the p x p factor R0 of A_S (shifted
     // CholeskyQR3, tsqr.cu) instead of the m x p sample itself.
     const bool tallq = m >= 8 * p && m >= 512 && p <= 1024;  // measured break-even is near m = 4p
+    // the m x p sample itself is factored only without the R0 route (or when
+    // that route falls back below): check its fit only then
+    const bool sample_fits = check_cpqr_fits(h, m, p, ch) == IDK_OK;
+    if (!tallq && !sample_fits) return IDK_ERR_INVALID_ARG;
     const CpqrChoice ch2 = tallq ? choose_cpqr(h, p, p, k) : ch;
     if (tallq && (rc = check_cpqr_fits(h, p, p, ch2))) return rc;
     const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(k), n, m, h->num_sms);
@@ -467,6 +482,9 @@ int sampled_rid(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t
             mc = p;
             chc = ch2;
             wc = w2;
+        } else if (!sample_fits) {
+            return set_err(h, IDK_ERR_INVALID_ARG,
+                           "optim_rid: the sample needs the m x p pivoted QR, which exceeds the on-chip CPQR budget");
         }
     }
     long long* piv = reinterpret_cast<long long*>(base + wc.pivots);
@@ -590,6 +608,9 @@ int idk_destroy(idk_handle h) {
     for (cudaEvent_t e : h->ev_io) cudaEventDestroy(e);
     if (h->s_in) cudaStreamDestroy(h->s_in);
     if (h->s_out) cudaStreamDestroy(h->s_out);
+    if (h->nccl_comm && h->nccl_owned) {
+        if (const idk::NcclApi* api = idk::nccl_api(nullptr)) api->CommDestroy(h->nccl_comm);
+    }
     delete h;
     return IDK_OK;
 }
@@ -607,6 +628,12 @@ int64_t idk_kernel_launches(idk_handle h) { return h ? h->launches : 0; }
 int idk_set_cpqr_mode(idk_handle h, int mode) {
     if (!h || mode < IDK_CPQR_AUTO || mode > IDK_CPQR_CLUSTER_PULL) return IDK_ERR_INVALID_ARG;
     h->cpqr_mode = mode;
+    return IDK_OK;
+}
+
+int idk_set_sketch_order(idk_handle h, int order) {
+    if (!h || (order != IDK_SKETCH_DMMA && order != IDK_SKETCH_REFERENCE_ORDER)) return IDK_ERR_INVALID_ARG;
+    h->sketch_order = order;
     return IDK_OK;
 }
 
@@ -932,7 +959,7 @@ int idk_id_from_sketch(idk_handle h, double* d_y, int64_t l, int64_t n, int64_t 
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     int* status = reinterpret_cast<int*>(base + w.status);
     IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
-    IDK_CUDA(run_cpqr(h, ch, d_y, l, n, k, base, w));
+    IDK_CUDA(run_cpqr(h, ch, d_y, l, n, k, base, w, ldy));
     h->launches += 1;
     // R11 + the local column range of Z only (columns are independent).
     IDK_CUDA(idk::id_solve_z(d_y, ldy, static_cast<int>(k), c_begin, c_end - c_begin, piv, pos,
@@ -966,6 +993,14 @@ int idk_diagnostics(idk_handle h, const double* d_a, int64_t m, int64_t n, int64
     // M: the decomposed matrix (A, or A^T for the dual); C is M's column subset.
     const int64_t mr = transposed ? n : m, mc = transposed ? m : n;
     if (mr > INT_MAX) return set_err(h, IDK_ERR_INVALID_ARG, "diagnostics: dimension too large");
+    {  // id.cpp:108-111: an index outside the coefficient matrix is invalid_argument
+        std::vector<int64_t> hc(static_cast<size_t>(k));
+        IDK_CUDA(cudaMemcpyAsync(hc.data(), d_cols, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->stream));
+        IDK_CUDA(cudaStreamSynchronize(h->stream));
+        for (int64_t c : hc)
+            if (c < 0 || c >= mc)
+                return set_err(h, IDK_ERR_INVALID_ARG, "diagnostics: column index outside coefficient matrix");
+    }
     Carve cv;
     const size_t cofs = d_c ? 0 : cv.take(sizeof(double) * mr * k);
     const size_t pofs = cv.take(sizeof(double) * idk::resid_partials(static_cast<int>(mr), mc));
@@ -1454,6 +1489,174 @@ int idk_id_auto_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int6
     IDK_CUDA(cudaMemcpyAsync(h_z, d_z, sizeof(double) * k * zc, cudaMemcpyDeviceToHost, h->stream));
     if (h_c) IDK_CUDA(cudaMemcpyAsync(h_c, d_c, sizeof(double) * crow * k, cudaMemcpyDeviceToHost, h->stream));
     IDK_CUDA(cudaStreamSynchronize(h->stream));
+    return IDK_OK;
+}
+
+// ---- multi-GPU: column-sharded ID over NCCL ----------
+
+int idk_shard_range(int64_t n, int nranks, int rank, int64_t* begin, int64_t* end) {
+    if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || !begin || !end) return IDK_ERR_INVALID_ARG;
+    const int64_t w = (n + nranks - 1) / nranks;
+    *begin = std::min<int64_t>(static_cast<int64_t>(rank) * w, n);
+    *end = std::min<int64_t>(*begin + w, n);
+    return IDK_OK;
+}
+
+int idk_nccl_unique_id(void* out128) {
+    if (!out128) return IDK_ERR_INVALID_ARG;
+    std::string e;
+    const idk::NcclApi* api = idk::nccl_api(&e);
+    if (!api) return IDK_ERR_NCCL;
+    idk::ncclUniqueId id;
+    if (api->GetUniqueId(&id) != 0) return IDK_ERR_NCCL;
+    std::memcpy(out128, id.internal, sizeof(id.internal));
+    return IDK_OK;
+}
+
+int idk_comm_init(idk_handle h, int nranks, int rank, const void* id128) {
+    if (!h || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return IDK_ERR_INVALID_ARG;
+    std::string e;
+    const idk::NcclApi* api = idk::nccl_api(&e);
+    if (!api) return set_err(h, IDK_ERR_NCCL, "comm_init: " + e);
+    cudaSetDevice(h->device);
+    if (h->nccl_comm && h->nccl_owned) api->CommDestroy(h->nccl_comm);
+    h->nccl_comm = nullptr;
+    idk::ncclUniqueId id;
+    std::memcpy(id.internal, id128, sizeof(id.internal));
+    idk::ncclComm_t c = nullptr;
+    const idk::ncclResult_t r = api->CommInitRank(&c, nranks, id, rank);
+    if (r != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclCommInitRank: ") + api->GetErrorString(r));
+    h->nccl_comm = c;
+    h->nccl_owned = true;
+    h->nranks = nranks;
+    h->rank = rank;
+    return IDK_OK;
+}
+
+int idk_set_nccl_comm(idk_handle h, void* nccl_comm) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    std::string e;
+    const idk::NcclApi* api = idk::nccl_api(&e);
+    if (!api) return set_err(h, IDK_ERR_NCCL, "set_nccl_comm: " + e);
+    if (h->nccl_comm && h->nccl_owned) api->CommDestroy(h->nccl_comm);
+    h->nccl_comm = static_cast<idk::ncclComm_t>(nccl_comm);
+    h->nccl_owned = false;
+    h->nranks = 1;
+    h->rank = 0;
+    if (h->nccl_comm) {
+        int cnt = 0, rk = 0;
+        if (api->CommCount(h->nccl_comm, &cnt) != 0 || api->CommUserRank(h->nccl_comm, &rk) != 0)
+            return set_err(h, IDK_ERR_NCCL, "set_nccl_comm: communicator query failed");
+        h->nranks = cnt;
+        h->rank = rk;
+    }
+    return IDK_OK;
+}
+
+int idk_comm_destroy(idk_handle h) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    if (h->nccl_comm && h->nccl_owned) {
+        if (const idk::NcclApi* api = idk::nccl_api(nullptr)) api->CommDestroy(h->nccl_comm);
+    }
+    h->nccl_comm = nullptr;
+    h->nccl_owned = false;
+    h->nranks = 1;
+    h->rank = 0;
+    return IDK_OK;
+}
+
+int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, int64_t lda, int a_transposed,
+                   int64_t k, int64_t p, uint64_t seed, int omega_mode, const double* d_omega, int64_t* d_cols,
+                   double* d_z_local, double* d_c) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    int rc = check_k(h, m, n, k, "id_sharded");
+    if (rc) return rc;
+    if (p < 0) return set_err(h, IDK_ERR_INVALID_ARG, "id_sharded: oversampling p must be non-negative");
+    if (omega_mode < 0 || omega_mode > 2 || (omega_mode == IDK_OMEGA_VERBATIM && !d_omega))
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_sharded: bad omega mode");
+    const int G = h->nranks, r = h->rank;
+    const idk::NcclApi* api = nullptr;
+    if (G > 1) {
+        std::string e;
+        if (!h->nccl_comm || !(api = idk::nccl_api(&e)))
+            return set_err(h, IDK_ERR_NCCL, "id_sharded: no NCCL communicator (idk_comm_init) " + e);
+    }
+    int64_t b = 0, e_ = 0;
+    idk_shard_range(n, G, r, &b, &e_);
+    const int64_t w = (n + G - 1) / G, nr = e_ - b;
+    const bool trans = a_transposed != 0;
+    if (nr > 0 && (!d_a_local || lda < (trans ? nr : m)))
+        return set_err(h, IDK_ERR_INVALID_ARG, "id_sharded: bad local block or leading dimension");
+    if (!d_cols || (nr > 0 && !d_z_local)) return set_err(h, IDK_ERR_INVALID_ARG, "id_sharded: null output");
+    const int64_t l = k + p;
+    const CpqrChoice ch = choose_cpqr(h, l, n, k);
+    if ((rc = check_cpqr_fits(h, l, n, ch))) return rc;
+    const int splits = nr > 0 ? idk::sketch_gemm_pick_splits(static_cast<int>(l), nr, m, h->num_sms) : 1;
+    Carve cv;
+    const size_t oofs = omega_mode == IDK_OMEGA_VERBATIM ? 0 : cv.take(sizeof(double) * l * m);
+    const size_t yofs = cv.take(sizeof(double) * l * w * G);  // rank q's block at column q*w: one in-place all-gather
+    const size_t pofs = splits > 1 ? cv.take(sizeof(double) * l * nr * splits) : 0;
+    const CpqrWs ws = carve_cpqr(cv, l, n, k, h->num_sms, ch);
+    if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
+    const double* omega = d_omega;
+    if (omega_mode != IDK_OMEGA_VERBATIM) {
+        double* om = reinterpret_cast<double*>(h->ws + oofs);
+        if (omega_mode == IDK_OMEGA_PHILOX) {
+            IDK_CUDA(idk::omega_philox(om, l, m, seed, h->stream));
+        } else {  // the reference's generate(gaussian) stream on the host (same on every rank)
+            std::vector<double> hv(static_cast<size_t>(l * m));
+            host_generate_gaussian(hv.data(), l * m, seed);
+            IDK_CUDA(cudaMemcpyAsync(om, hv.data(), sizeof(double) * l * m, cudaMemcpyHostToDevice, h->stream));
+            IDK_CUDA(cudaStreamSynchronize(h->stream));
+        }
+        h->launches += omega_mode == IDK_OMEGA_PHILOX ? 1 : 0;
+        omega = om;
+    }
+    double* Y = reinterpret_cast<double*>(h->ws + yofs);
+    if (nr > 0) {  // this rank's columns of Y = Omega M, straight into its slot of the gathered Y
+        IDK_CUDA(idk::sketch_gemm(omega, l, d_a_local, lda, trans, Y + b * l, l, static_cast<int>(l), nr, m, splits,
+                                  splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr, h->stream));
+        h->launches += splits > 1 ? 2 : 1;
+    }
+    if (G > 1) {
+        const idk::ncclResult_t nr_ = api->AllGather(Y + static_cast<int64_t>(r) * w * l, Y, static_cast<size_t>(w * l),
+                                                    idk::kNcclFloat64, h->nccl_comm, h->stream);
+        if (nr_ != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllGather: ") + api->GetErrorString(nr_));
+    }
+    // replicated deterministic CPQR: bit-identical on every rank, so no broadcast of the pivots
+    long long* pos = reinterpret_cast<long long*>(h->ws + ws.pos);
+    long long* piv = reinterpret_cast<long long*>(h->ws + ws.pivots);
+    int* status = reinterpret_cast<int*>(h->ws + ws.status);
+    IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
+    IDK_CUDA(run_cpqr(h, ch, Y, l, n, k, h->ws, ws));
+    IDK_CUDA(idk::id_solve_z(Y, l, static_cast<int>(k), b, nr, piv, pos, reinterpret_cast<double*>(h->ws + ws.r11),
+                             status, d_z_local, h->stream));
+    h->launches += nr > 0 ? 3 : 2;
+    IDK_CUDA(cudaMemcpyAsync(d_cols, piv, sizeof(long long) * k, cudaMemcpyDeviceToDevice, h->stream));
+    std::vector<int64_t> hcols(static_cast<size_t>(k));
+    IDK_CUDA(cudaMemcpyAsync(hcols.data(), piv, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaMemcpyAsync(h->h_status, status, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    if (d_c && nr > 0) {  // the selected columns this rank owns
+        IDK_CUDA(idk::gather_owned(d_a_local, lda, m, piv, static_cast<int>(k), b, e_, trans, d_c, h->stream));
+        h->launches += 1;
+    }
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    if (*h->h_status != 0x7f7f7f7f)
+        return set_err(h, IDK_ERR_SINGULAR, "solve_triangular: zero diagonal at index " + std::to_string(*h->h_status));
+    if (d_c && G > 1) {  // each column of C comes from its one owner: exact, no reduction
+        for (int64_t j0 = 0; j0 < k; j0 += 512) {
+            api->GroupStart();
+            for (int64_t j = j0; j < std::min<int64_t>(k, j0 + 512); ++j) {
+                double* col = d_c + j * m;
+                api->Broadcast(col, col, static_cast<size_t>(m), idk::kNcclFloat64, static_cast<int>(hcols[j] / w),
+                               h->nccl_comm, h->stream);
+            }
+            const idk::ncclResult_t gr = api->GroupEnd();
+            if (gr != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclBroadcast: ") + api->GetErrorString(gr));
+        }
+        IDK_CUDA(cudaStreamSynchronize(h->stream));
+    }
     return IDK_OK;
 }
 

@@ -74,6 +74,8 @@ cudaError_t gather_columns(const double* A, int64_t lda, int64_t rows, const lon
                            double* C, cudaStream_t stream);
 cudaError_t gather_r11(const double* W, int64_t ldw, const long long* pivots, int k, double* R11,
                        cudaStream_t stream);
+cudaError_t gather_owned(const double* A, int64_t lda, int64_t rows, const long long* cols, int k, int64_t c_begin,
+                         int64_t c_end, bool rows_of_a, double* C, cudaStream_t stream);
 cudaError_t copy_pivots(const long long* src, int k, long long* dst, cudaStream_t stream);
 
 // batched.cu
@@ -101,7 +103,7 @@ cudaError_t gram_trace(const double* G, int p, double* out, int* zero_col, cudaS
 
 // util.cu
 cudaError_t matmul_ref_order(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M, int64_t N, int K,
-                             double* C, int64_t ldc, cudaStream_t stream);
+                             double* C, int64_t ldc, cudaStream_t stream, bool b_trans = false);
 cudaError_t transpose_copy(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb,
                            cudaStream_t stream);
 

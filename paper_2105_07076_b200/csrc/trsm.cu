@@ -553,6 +553,20 @@ __global__ void gather_rows_kernel(const double* __restrict__ A, int64_t lda, in
     for (int j = wid; j < k; j += nw)
         if (i < n) __stcs(C + static_cast<int64_t>(j) * n + i, tile[j * 33 + lane]);
 }
+// Sharded C: this rank holds columns [c_begin, c_end) of M (A_local, or the
+// row block of the stored tall A for the dual).  Column j of C is written here
+// only when its pivot is local; the owners' broadcasts fill the rest.
+__global__ void gather_owned_kernel(const double* __restrict__ A, int64_t lda, int64_t rows,
+                                    const long long* __restrict__ cols, int64_t c_begin, int64_t c_end, bool rows_of_a,
+                                    double* __restrict__ C) {
+    const int j = blockIdx.y;
+    const long long g = cols[j];
+    if (g < c_begin || g >= c_end) return;
+    const int64_t loc = g - c_begin;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        C[static_cast<int64_t>(j) * rows + i] = rows_of_a ? A[loc + i * lda] : A[loc * lda + i];
+}
 __global__ void copy_pivots_kernel(const long long* __restrict__ src, int k, long long* __restrict__ dst) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
@@ -663,6 +677,14 @@ cudaError_t gather_columns(const double* A, int64_t lda, int64_t rows, const lon
     }
     gather_columns_kernel<<<static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8)), 256, 0, stream>>>(
         A, lda, rows, cols, k, rows_of_a, C);
+    return cudaGetLastError();
+}
+
+cudaError_t gather_owned(const double* A, int64_t lda, int64_t rows, const long long* cols, int k, int64_t c_begin,
+                         int64_t c_end, bool rows_of_a, double* C, cudaStream_t stream) {
+    if (rows <= 0 || k <= 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((rows + 255) / 256, 64)), static_cast<unsigned>(k));
+    gather_owned_kernel<<<grid, 256, 0, stream>>>(A, lda, rows, cols, c_begin, c_end, rows_of_a, C);
     return cudaGetLastError();
 }
 

@@ -1,5 +1,7 @@
 // util.cu -- layout helpers for the id_auto dual (id.cpp:85: transpose(a)) and
 // the reference-order product used for IdResult::approx.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace idk {
@@ -26,18 +28,20 @@ __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int6
 // skipping b(l,j) == 0, with unfused IEEE multiply and add (the reference is
 // built without FMA).  Bit-identical to the reference's matmul; one thread per
 // output, rows across lanes (coalesced A, broadcast B).
+// b_trans: B(l, j) = B[j + l * ldb] (the sketch of the id_auto dual reads the
+// stored tall A transposed, like matmul(Omega, transpose(A))).
 __global__ void matmul_ref_order_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
-                                        int64_t ldb, int64_t M, int64_t N, int K, double* __restrict__ C,
-                                        int64_t ldc) {
+                                        int64_t ldb, bool b_trans, int64_t M, int64_t N, int K,
+                                        double* __restrict__ C, int64_t ldc) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t j = blockIdx.y;
-    if (j >= N) return;
-    const double* bj = B + j * ldb;
-    double acc = 0.0;
-    if (i < M) {
-        const double* ai = A + i;
+    if (i >= M) return;
+    const double* ai = A + i;
+    for (int64_t j = blockIdx.y; j < N; j += gridDim.y) {  // N may exceed the 65535 grid rows
+        const double* bj = b_trans ? B + j : B + j * ldb;
+        const int64_t bstep = b_trans ? ldb : 1;
+        double acc = 0.0;
         for (int l = 0; l < K; ++l) {
-            const double b = __ldg(bj + l);
+            const double b = __ldg(bj + l * bstep);
             if (b == 0.0) continue;
             acc = __dadd_rn(acc, __dmul_rn(ai[static_cast<int64_t>(l) * lda], b));
         }
@@ -47,10 +51,10 @@ __global__ void matmul_ref_order_kernel(const double* __restrict__ A, int64_t ld
 }  // namespace
 
 cudaError_t matmul_ref_order(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t M, int64_t N, int K,
-                             double* C, int64_t ldc, cudaStream_t stream) {
+                             double* C, int64_t ldc, cudaStream_t stream, bool b_trans) {
     if (M <= 0 || N <= 0) return cudaSuccess;
-    dim3 grid(static_cast<unsigned>((M + 127) / 128), static_cast<unsigned>(N));
-    matmul_ref_order_kernel<<<grid, 128, 0, stream>>>(A, lda, B, ldb, M, N, K, C, ldc);
+    dim3 grid(static_cast<unsigned>((M + 127) / 128), static_cast<unsigned>(std::min<int64_t>(N, 65535)));
+    matmul_ref_order_kernel<<<grid, 128, 0, stream>>>(A, lda, B, ldb, b_trans, M, N, K, C, ldc);
     return cudaGetLastError();
 }
 

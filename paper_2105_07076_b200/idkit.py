@@ -120,6 +120,13 @@ class Context:
     def set_cpqr_mode(self, mode: int):
         self.check(self.lib.idk_set_cpqr_mode(self.h, mode))
 
+    SKETCH_DMMA, SKETCH_REFERENCE_ORDER = 0, 1
+
+    def set_sketch_order(self, order: int):
+        """IDK_SKETCH_DMMA (default) or IDK_SKETCH_REFERENCE_ORDER (Y bit-identical to the
+        reference's matmul, matrix.cpp:28-48; slow -- bit-compatibility checks)."""
+        self.check(self.lib.idk_set_sketch_order(self.h, order))
+
     def set_batched_exact(self, exact: bool = True):
         self.check(self.lib.idk_set_batched_exact(self.h, 1 if exact else 0))
 
@@ -139,6 +146,18 @@ class Context:
         buf = (C.c_double * 5)()
         n = self.lib.idk_stage_times(self.h, buf, 5)
         return {self.STAGES[i]: buf[i] for i in range(n)}
+
+    # ---- multi-GPU: the handle's NCCL communicator (idk_comm_init) ----
+    def comm_init(self, nranks: int, rank: int, unique_id: bytes):
+        if len(unique_id) != 128:
+            raise InvalidArgument("an ncclUniqueId is 128 bytes")
+        buf = C.create_string_buffer(unique_id, 128)
+        self.check(self.lib.idk_comm_init(self.h, nranks, rank, buf))
+        self.nranks, self.rank = nranks, rank
+
+    def comm_destroy(self):
+        self.check(self.lib.idk_comm_destroy(self.h))
+        self.nranks, self.rank = 1, 0
 
 
 _tls = threading.local()
@@ -456,6 +475,52 @@ def diagnostics(a, r: IdResult) -> dict:
                                       _ptr(z), cptr, out))
     return {"relative_error": out[0], "max_abs_z": out[1], "identity_deviation": out[2],
             "entry_bound_satisfied": bool(out[3])}
+
+
+# ---- multi-GPU (C ABI: idk_shard_range / idk_comm_init / idk_id_sharded) ------------
+
+def shard_range(n: int, nranks: int, rank: int):
+    """Columns [begin, end) of an n-column matrix owned by `rank` (ceil-sized blocks)."""
+    lib = _lib.load()
+    b, e = C.c_int64(), C.c_int64()
+    if lib.idk_shard_range(n, nranks, rank, C.byref(b), C.byref(e)) != 0:
+        raise InvalidArgument("shard_range: bad arguments")
+    return b.value, e.value
+
+
+def nccl_unique_id() -> bytes:
+    lib = _lib.load()
+    buf = C.create_string_buffer(128)
+    rc = lib.idk_nccl_unique_id(buf)
+    if rc != 0:
+        raise CudaError("idk_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+def id_sharded(a_local, m: int, n: int, k: int, p: int, seed: int = 0, transposed: bool = False,
+               omega_mode: int = OMEGA_PHILOX, omega=None, want_c: bool = True):
+    """Column-sharded sketch RID through the C ABI (idk_id_sharded) on this
+    rank's context (comm_init first for more than one rank).  a_local: this
+    rank's columns of M (m x n_r), or with transposed=True the stored row block
+    (n_r x m) of the tall A.  Returns (cols, z_local (k x n_r), c (m x k))."""
+    import torch
+    dev = a_local.device
+    ctx = context(dev.index or 0)
+    ctx.bind_stream()
+    a_local = fortran(a_local)
+    nranks, rank = getattr(ctx, "nranks", 1), getattr(ctx, "rank", 0)
+    b, e = shard_range(n, nranks, rank)
+    nr = e - b
+    if (a_local.shape[0] if transposed else a_local.shape[1]) != nr:
+        raise InvalidArgument(f"rank {rank}: local block has the wrong width (expected {nr} columns of M)")
+    om = fortran(omega) if omega is not None else None
+    cols = torch.empty(max(k, 0), dtype=torch.int64, device=dev)
+    z = empty_f(max(k, 0), nr, dev)
+    c = empty_f(m, max(k, 0), dev) if want_c else None
+    ctx.check(ctx.lib.idk_id_sharded(ctx.h, _ptr(a_local) if nr > 0 else None, m, n, _ld(a_local) if nr > 0 else 1,
+                                     1 if transposed else 0, k, p, seed, omega_mode, _ptr(om), _ptr(cols),
+                                     _ptr(z) if nr > 0 else None, _ptr(c)))
+    return cols, z, c
 
 
 # ---- stages / primitives ----------------------------------------------------------

@@ -39,3 +39,46 @@ def rel(a, b):
     d = np.linalg.norm(a - b)
     nb = np.linalg.norm(b)
     return d / nb if nb > 0 else d
+
+
+# ---- parity records (profiles/parity_r02.json is copied from this file) ----------
+_PARITY = {}
+
+
+@pytest.fixture(scope="session")
+def parity_record():
+    """Tests add one dict per config; written to gpurun_out/parity_records.json
+    at the end of the session (pivot equality, ||dZ||/||Z||, relative errors,
+    reference wall time)."""
+    return _PARITY
+
+
+def pytest_sessionfinish(session, exitstatus):
+    if not _PARITY:
+        return
+    import json
+    import platform
+    out = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    path = os.path.join(out, "parity_records.json")
+    old = {}
+    try:
+        with open(path) as f:
+            old = json.load(f)
+    except (OSError, ValueError):
+        pass
+    old.update(_PARITY)
+    old["_host"] = {"nproc": os.cpu_count(), "cpu": _cpu_model(), "machine": platform.machine()}
+    with open(path, "w") as f:
+        json.dump(old, f, indent=1, sort_keys=True)
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"

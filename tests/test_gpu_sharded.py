@@ -65,3 +65,32 @@ def test_id_from_sketch_rejects_bad_range(oracle):
     y = dev(oracle.gaussian_matrix(30, 100, 1))
     with pytest.raises(idk.InvalidArgument):
         idk.id_from_sketch(y, 10, 50, 120)
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+def test_c_abi_id_sharded_one_rank(oracle, transposed):
+    """idk_id_sharded without a communicator (one rank) equals idk_sketch_rid bit for bit."""
+    import paper_2105_07076_b200 as idk
+    if transposed:
+        a = dev(oracle.gaussian_matrix(2600, 150, 6))
+        m, n = 150, 2600
+    else:
+        a = dev(oracle.gaussian_matrix(180, 3100, 6))
+        m, n = 180, 3100
+    cols, z, c = idk.id_sharded(a, m, n, 30, 8, seed=21, transposed=transposed)
+    ref = idk.sketch_rid(a, 30, 8, seed=21, transposed=transposed)
+    assert torch.equal(cols, ref.cols) and torch.equal(z, ref.z) and torch.equal(c, ref.c)
+
+
+def test_c_abi_id_sharded_one_rank_nccl_comm(oracle):
+    """The same through an NCCL communicator of size 1 (idk_nccl_unique_id + idk_comm_init)."""
+    import paper_2105_07076_b200 as idk
+    a = dev(oracle.gaussian_matrix(160, 2000, 8))
+    ctx = idk.context(0)
+    ctx.comm_init(1, 0, idk.nccl_unique_id())
+    try:
+        cols, z, c = idk.id_sharded(a, 160, 2000, 25, 5, seed=4)
+    finally:
+        ctx.comm_destroy()
+    ref = idk.sketch_rid(a, 25, 5, seed=4)
+    assert torch.equal(cols, ref.cols) and torch.equal(z, ref.z) and torch.equal(c, ref.c)

@@ -32,14 +32,21 @@ def _worker(rank, world, port, case, out_dir):
         from oracle import Oracle
         from paper_2105_07076_b200 import sharded
         o = Oracle()
-        if case in ("wide", "tall"):
-            m, n, k, p = (40, 97, 8, 3) if case == "wide" else (101, 30, 7, 2)
+        if case in ("wide", "tall", "narrow"):
+            m, n, k, p = {"wide": (40, 97, 8, 3), "tall": (101, 30, 7, 2), "narrow": (30, 9, 4, 2)}[case]
             a = o.gaussian_matrix(m, n, 5)
             a[:, ::4] *= 3.0
-            if case == "wide":
+            if case == "wide":  # a dominant column holding -0.0 entries: C must keep their sign
+                a[:, 9] *= 50.0
+                a[:4, 9] = -0.0
+            elif case == "tall":
+                a[17, :] *= 50.0
+                a[17, :3] = -0.0
+            if case in ("wide", "narrow"):
                 b, e = column_range(n, world, rank)
                 local = _t(a[:, b:e])
                 cols, z_local, c = sharded.sketch_rid_sharded(local, n, k, p, seed=11, stages=OracleStages())
+                assert z_local.shape == (k, e - b)
                 ntot = n
             else:  # M = A^T (30 x 101); rank owns rows [b, e) of A = columns of M
                 b, e = column_range(m, world, rank)
@@ -65,15 +72,19 @@ def _run(world, case, tmp_path):
 
 
 def test_column_range_covers_exactly():
-    for n in (1, 5, 97, 16384):
-        for world in (1, 2, 3, 8):
+    from paper_2105_07076_b200 import idkit
+    for n in (1, 5, 97, 16384, 65536):
+        for world in (1, 2, 3, 4, 8):
             spans = [column_range(n, world, r) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
-            assert max(e - b for b, e in spans) - min(e - b for b, e in spans) <= 1
+            w = -(-n // world)
+            assert all(b == min(r * w, n) and e - b <= w for r, (b, e) in enumerate(spans))
+            # the C ABI's split (idk_shard_range) is the same
+            assert spans == [idkit.shard_range(n, world, r) for r in range(world)]
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("case", ["wide", "tall"])
 def test_sharded_sketch_matches_single_process(world, case, tmp_path, oracle):
     _run(world, case, tmp_path)
@@ -86,6 +97,18 @@ def test_sharded_sketch_matches_single_process(world, case, tmp_path, oracle):
     assert np.array_equal(d["cols"], cols)
     assert np.array_equal(d["z"], z)
     assert np.array_equal(d["c"], c)
+    assert np.array_equal(np.signbit(d["c"]), np.signbit(c))  # -0.0 survives (no SUM all-reduce)
+    assert np.signbit(d["c"]).any()
+
+
+def test_sharded_with_an_empty_rank(tmp_path, oracle):
+    """9 columns over 4 ranks: blocks of 3, the last rank owns none but still
+    takes part in the all-gather and the broadcasts."""
+    _run(4, "narrow", tmp_path)
+    d = np.load(tmp_path / "narrow.npz")
+    om = oracle.omega_philox(6, 30, 11)
+    cols, z, c, _ = oracle.interp_decomp(d["a"], 4, om)
+    assert np.array_equal(d["cols"], cols) and np.array_equal(d["z"], z) and np.array_equal(d["c"], c)
 
 
 def test_batched_partition_by_matrix(tmp_path, oracle):
