@@ -300,6 +300,20 @@ IDK_API int idk_optim_id_host(idk_handle h, const double* h_a, int64_t m, int64_
 IDK_API int idk_optim_rid_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k,
                                double oversampling_fraction, uint64_t seed, int64_t* h_cols, double* h_z,
                                double* h_c, double* h_approx);
+/* idkit::id_auto with the reference's full value semantics (id.hpp:55-56,
+ * id.cpp:78-95), IdResult::approx included: method 0 = optim_id, 1 = the
+ * reference's randomized ID optim_rid (oversampling_fraction), 2 = the
+ * Gaussian-sketch RID (oversampling p, Philox Omega keyed by seed).  h_a is
+ * m x n (ld = m).  When m > n the ID runs on A^T with the device reading A
+ * transposed (no host transpose, unlike id.cpp:85): *transposed = 1, cols
+ * index rows of A, h_z is k x m, h_c (optional) n x k, and h_approx (optional,
+ * m x n) = transpose(matmul(C, Z)) as id.cpp:92 forms it.  approx is computed
+ * on the device in matmul's exact arithmetic (bit-identical to the
+ * reference's matmul of the same C and Z). */
+IDK_API int idk_id_auto_ref_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int method,
+                                 uint64_t seed, double oversampling_fraction, int64_t p, int64_t* h_cols, double* h_z,
+                                 double* h_c, double* h_approx, int* transposed);
+
 /* idkit::matmul (matrix.hpp:56, matrix.cpp:28-48) in the reference's exact
  * arithmetic (same summation order, zero skipping, unfused IEEE ops):
  * C (m x n, ldc) = A (m x k, lda) * B (k x n, ldb), bit-identical to the CPU

@@ -8,7 +8,8 @@
 //   id_auto             id.hpp:55-56   (id.cpp:78-95)
 //   diagnostics         id.hpp:60      (id.cpp:97-122)
 //   qr_column_pivoted   qr.hpp:34      (qr.cpp:42-126)
-// -- and forwards the work to the C ABI of libidkit_b200.so
+// -- adds the north-star Gaussian-sketch RID as idkit::sketch_rid
+// (integration/idkit_b200_ext.hpp) -- and forwards the work to the C ABI of libidkit_b200.so
 // (include/idkit_b200.h).  Everything else (Matrix, matmul, the solvers, svd,
 // datasets, bench's run_cell, acceptance) is the reference's code, unchanged,
 // so its callers relink without edits (oracle/Makefile target `dropin`).
@@ -32,6 +33,7 @@
 #include "idkit/matrix.hpp"
 #include "idkit/qr.hpp"
 #include "idkit_b200.h"
+#include "idkit_b200_ext.hpp"
 
 namespace idkit {
 
@@ -98,18 +100,36 @@ IdResult optim_rid(const Matrix& a, std::size_t k, double oversampling_fraction,
     return finish(cols, std::move(z), std::move(approx));
 }
 
+// id.cpp:78-95 in one device call: for a tall a (m > n) the device reads a
+// transposed (no host transpose, unlike id.cpp:85) and forms approx as
+// transpose(matmul(C, Z)) (id.cpp:92) in matmul's exact arithmetic.
 IdResult id_auto(const Matrix& a, std::size_t k, IdMethod method, std::uint64_t seed, double oversampling_fraction) {
     rank_contract(a, k, "id_auto");
-    if (a.rows() <= a.cols()) {
-        return method == IdMethod::deterministic ? optim_id(a, k) : optim_rid(a, k, oversampling_fraction, seed);
-    }
-    const Matrix at = transpose(a);
-    IdResult dual = method == IdMethod::deterministic ? optim_id(at, k) : optim_rid(at, k, oversampling_fraction, seed);
-    IdResult out;
-    out.cols = std::move(dual.cols);  // row indices of a
-    out.z = std::move(dual.z);
-    out.approx = transpose(dual.approx);
-    out.transposed = true;
+    if (method != IdMethod::deterministic && !(oversampling_fraction >= 0.0))
+        throw std::invalid_argument("optim_rid: oversampling_fraction must be non-negative");
+    const bool dual = a.rows() > a.cols();
+    std::vector<int64_t> cols(k);
+    Matrix z(k, dual ? a.rows() : a.cols()), approx(a.rows(), a.cols());
+    int tr = 0;
+    check(idk_id_auto_ref_host(handle(), a.data(), static_cast<int64_t>(a.rows()), static_cast<int64_t>(a.cols()),
+                               static_cast<int64_t>(k), method == IdMethod::deterministic ? 0 : 1, seed,
+                               oversampling_fraction, 0, cols.data(), z.data(), nullptr, approx.data(), &tr));
+    IdResult out = finish(cols, std::move(z), std::move(approx));
+    out.transposed = tr != 0;  // cols are row indices of a
+    return out;
+}
+
+IdResult sketch_rid(const Matrix& a, std::size_t k, std::size_t oversampling, std::uint64_t seed) {
+    rank_contract(a, k, "sketch_rid");
+    const bool dual = a.rows() > a.cols();
+    std::vector<int64_t> cols(k);
+    Matrix z(k, dual ? a.rows() : a.cols()), approx(a.rows(), a.cols());
+    int tr = 0;
+    check(idk_id_auto_ref_host(handle(), a.data(), static_cast<int64_t>(a.rows()), static_cast<int64_t>(a.cols()),
+                               static_cast<int64_t>(k), 2, seed, 0.0, static_cast<int64_t>(oversampling), cols.data(),
+                               z.data(), nullptr, approx.data(), &tr));
+    IdResult out = finish(cols, std::move(z), std::move(approx));
+    out.transposed = tr != 0;
     return out;
 }
 

@@ -37,6 +37,8 @@ SIGNATURES = {
     "idk_qr_column_pivoted_host": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _P, _P]),
     "idk_optim_id_host": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _P, _P, _P]),
     "idk_optim_rid_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_double, C.c_uint64, _P, _P, _P, _P]),
+    "idk_id_auto_ref_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, C.c_uint64, C.c_double, _I64, _P, _P, _P,
+                                       _P, C.POINTER(C.c_int)]),
     "idk_matmul_ref": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64]),
     "idk_optim_rid": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _I64, C.c_double, C.c_uint64, _P, _P, _P]),
     "idk_id_auto": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P, _P,

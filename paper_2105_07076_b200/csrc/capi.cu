@@ -1396,42 +1396,63 @@ int idk_id_auto_batch(idk_handle h, int64_t count, const double* const* d_a, int
 // Host-buffer forms of idk_optim_id / idk_optim_rid (value semantics of
 // id.hpp:40,47-48): A uploaded, the ID computed on the handle's stream, cols /
 // Z / C downloaded.  `rid` selects the column-sampling estimator.
-static int host_optim(idk_handle h, bool rid, const double* h_a, int64_t m, int64_t n, int64_t k, double frac,
-                      uint64_t seed, int64_t* h_cols, double* h_z, double* h_c, double* h_approx) {
+// Host-buffer ID with the reference's value semantics, IdResult included:
+// method 0 optim_id, 1 optim_rid (oversampling fraction), 2 the Gaussian-sketch
+// RID (p).  dual = true decomposes M = A^T of the tall host matrix A (m x n)
+// with the device reading A transposed -- id_auto's dual (id.cpp:78-95)
+// without the host transpose of id.cpp:85 -- and returns approx (m x n) =
+// transpose(matmul(C, Z)) as id.cpp:92 does; approx is always formed on the
+// device in matmul's exact arithmetic (matrix.cpp:28-48), so it is
+// bit-identical to the reference's product of the same C and Z.
+static int host_id(idk_handle h, int method, bool dual, const double* h_a, int64_t m, int64_t n, int64_t k,
+                   double frac, int64_t p, uint64_t seed, int64_t* h_cols, double* h_z, double* h_c,
+                   double* h_approx) {
     if (!h) return IDK_ERR_INVALID_ARG;
     cudaSetDevice(h->device);
-    int rc = check_k(h, m, n, k, rid ? "optim_rid" : "optim_id");
+    static const char* names[3] = {"optim_id", "optim_rid", "sketch_rid"};
+    if (method < 0 || method > 2) return set_err(h, IDK_ERR_INVALID_ARG, "id: method must be 0, 1 or 2");
+    int rc = check_k(h, m, n, k, names[method]);
     if (rc) return rc;
     if (!h_a || !h_cols || !h_z) return set_err(h, IDK_ERR_INVALID_ARG, "optim: null pointer");
-    if (rid && !(frac >= 0.0))
+    if (method == 1 && !(frac >= 0.0))
         return set_err(h, IDK_ERR_INVALID_ARG, "optim_rid: oversampling_fraction must be non-negative");
+    // M (mr x mc) is A, or A^T for the dual
+    const int64_t mr = dual ? n : m, mc = dual ? m : n;
     Carve cv;
     const size_t aofs = cv.take(sizeof(double) * m * n);
     const size_t cofs = cv.take(sizeof(int64_t) * k);
-    const size_t zofs = cv.take(sizeof(double) * k * n);
-    const size_t ccofs = cv.take(sizeof(double) * m * k);
+    const size_t zofs = cv.take(sizeof(double) * k * mc);
+    const size_t ccofs = cv.take(sizeof(double) * mr * k);
     const size_t apofs = h_approx ? cv.take(sizeof(double) * m * n) : 0;
+    const size_t tpofs = h_approx && dual ? cv.take(sizeof(double) * m * n) : 0;
     if ((rc = ensure(h, &h->io, &h->io_cap, cv.total))) return rc;
     double* d_a = reinterpret_cast<double*>(h->io + aofs);
     int64_t* d_cols = reinterpret_cast<int64_t*>(h->io + cofs);
     double* d_z = reinterpret_cast<double*>(h->io + zofs);
     double* d_c = (h_c || h_approx) ? reinterpret_cast<double*>(h->io + ccofs) : nullptr;
     IDK_CUDA(cudaMemcpyAsync(d_a, h_a, sizeof(double) * m * n, cudaMemcpyHostToDevice, h->stream));
-    if (rid) {
+    if (method == 1) {
         const double extra = frac * static_cast<double>(k);
         const int64_t e = extra >= 9.0e18 ? INT64_MAX / 2 : static_cast<int64_t>(static_cast<uint64_t>(extra));
-        rc = sampled_rid(h, d_a, m, n, m, false, k, e, seed, d_cols, d_z, d_c);
+        rc = sampled_rid(h, d_a, mr, mc, m, dual, k, e, seed, d_cols, d_z, d_c);
+    } else if (method == 2) {
+        rc = sketch_rid(h, d_a, mr, mc, m, dual, k, p, seed, IDK_OMEGA_PHILOX, nullptr, d_cols, d_z, d_c);
     } else {
-        rc = det_id(h, d_a, m, n, m, false, k, d_cols, d_z, d_c);
+        rc = det_id(h, d_a, mr, mc, m, dual, k, d_cols, d_z, d_c);
     }
     if (rc) return rc;
     IDK_CUDA(cudaMemcpyAsync(h_cols, d_cols, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, h->stream));
-    IDK_CUDA(cudaMemcpyAsync(h_z, d_z, sizeof(double) * k * n, cudaMemcpyDeviceToHost, h->stream));
-    if (h_c) IDK_CUDA(cudaMemcpyAsync(h_c, d_c, sizeof(double) * m * k, cudaMemcpyDeviceToHost, h->stream));
-    if (h_approx) {  // id.cpp:42,73: approx = matmul(C, Z), in the reference's exact arithmetic
+    IDK_CUDA(cudaMemcpyAsync(h_z, d_z, sizeof(double) * k * mc, cudaMemcpyDeviceToHost, h->stream));
+    if (h_c) IDK_CUDA(cudaMemcpyAsync(h_c, d_c, sizeof(double) * mr * k, cudaMemcpyDeviceToHost, h->stream));
+    if (h_approx) {  // id.cpp:42,73 (and :92 for the dual): approx = matmul(C, Z), exact arithmetic
         double* d_ap = reinterpret_cast<double*>(h->io + apofs);
-        IDK_CUDA(idk::matmul_ref_order(d_c, m, d_z, k, m, n, static_cast<int>(k), d_ap, m, h->stream));
+        double* d_prod = dual ? reinterpret_cast<double*>(h->io + tpofs) : d_ap;
+        IDK_CUDA(idk::matmul_ref_order(d_c, mr, d_z, k, mr, mc, static_cast<int>(k), d_prod, mr, h->stream));
         h->launches += 1;
+        if (dual) {
+            IDK_CUDA(idk::transpose_copy(d_prod, mr, mr, mc, d_ap, m, h->stream));
+            h->launches += 1;
+        }
         IDK_CUDA(cudaMemcpyAsync(h_approx, d_ap, sizeof(double) * m * n, cudaMemcpyDeviceToHost, h->stream));
     }
     IDK_CUDA(cudaStreamSynchronize(h->stream));
@@ -1440,12 +1461,20 @@ static int host_optim(idk_handle h, bool rid, const double* h_a, int64_t m, int6
 
 int idk_optim_id_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int64_t* h_cols, double* h_z,
                       double* h_c, double* h_approx) {
-    return host_optim(h, false, h_a, m, n, k, 0.0, 0, h_cols, h_z, h_c, h_approx);
+    return host_id(h, 0, false, h_a, m, n, k, 0.0, 0, 0, h_cols, h_z, h_c, h_approx);
 }
 
 int idk_optim_rid_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, double oversampling_fraction,
                        uint64_t seed, int64_t* h_cols, double* h_z, double* h_c, double* h_approx) {
-    return host_optim(h, true, h_a, m, n, k, oversampling_fraction, seed, h_cols, h_z, h_c, h_approx);
+    return host_id(h, 1, false, h_a, m, n, k, oversampling_fraction, 0, seed, h_cols, h_z, h_c, h_approx);
+}
+
+int idk_id_auto_ref_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int64_t k, int method, uint64_t seed,
+                         double oversampling_fraction, int64_t p, int64_t* h_cols, double* h_z, double* h_c,
+                         double* h_approx, int* transposed) {
+    const bool dual = m > n;  // id.cpp:84
+    if (transposed) *transposed = dual ? 1 : 0;
+    return host_id(h, method, dual, h_a, m, n, k, oversampling_fraction, p, seed, h_cols, h_z, h_c, h_approx);
 }
 
 int idk_matmul_ref(idk_handle h, const double* d_a, int64_t m, int64_t k, int64_t lda, const double* d_b, int64_t n,

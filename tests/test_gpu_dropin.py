@@ -80,3 +80,42 @@ def test_reference_acceptance_suite_through_the_shim():
     # criterion 7 (rand_id faster than det_id) is reported, not asserted: on the GPU both
     # are bound by the k dependent CPQR steps, see INTEGRATION.md
     assert "7" in status
+
+
+def test_shim_dual_and_sketch_rid_from_the_reference_side():
+    """integration/dropin_check.cpp: id_auto's dual without a host transpose and
+    idkit::sketch_rid, checked with the reference's own Matrix helpers."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_check_b200")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_check_b200 not built (make -C oracle dropin)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count("PASS") == 6
+
+
+@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("shape", [(90, 40), (40, 90)])
+def test_id_auto_ref_host_matches_reference_id_auto(idk, ref, method, shape):
+    """idk_id_auto_ref_host = idkit::id_auto (id.cpp:78-95) incl. approx, bit-identical
+    approx given the same (C, Z) -- the tall case without a host transpose."""
+    m, n = shape
+    a = np.asfortranarray(ref.gaussian_matrix(m, n, 21))
+    a[:, ::5] *= 3.0
+    k = 8
+    ctx = idk.context(0)
+    zc = max(m, n)
+    cols = np.empty(k, dtype=np.int64)
+    z = np.empty((k, zc), order="F")
+    approx = np.empty((m, n), order="F")
+    tr = C.c_int(0)
+    P = lambda x: x.ctypes.data_as(C.c_void_p)  # noqa: E731
+    ctx.check(ctx.lib.idk_id_auto_ref_host(ctx.h, P(a), m, n, k, method, 31, 0.25, 0, P(cols), P(z), None,
+                                           P(approx), C.byref(tr)))
+    rcols, rz, rapprox, rtr = ref.id_auto(a, k, method == 1, seed=31, frac=0.25)
+    assert bool(tr.value) == rtr == (m > n)
+    assert np.array_equal(cols, rcols)
+    assert np.linalg.norm(z - rz) <= 1e-10 * np.linalg.norm(rz)
+    mat = np.asfortranarray(a.T) if rtr else a
+    prod = ref.matmul(np.asfortranarray(mat[:, cols]), z)
+    assert np.array_equal(approx, np.asfortranarray(prod.T) if rtr else prod)
