@@ -165,10 +165,25 @@ CpqrChoice choose_cpqr(idk_context* h, int64_t mrows, int64_t n, int64_t k) {
 // Work buffers of one CPQR + Z solve on an m' x n matrix.
 struct CpqrWs {
     size_t pos, pivots, taus, pub, barrier, r11, status;
+    size_t xg = 0;  // streaming CPQR of a tall matrix: per-CTA reflector buffers in L2
+    bool has_xg = false;
 };
+
+// The streaming kernel keeps the reflector (m doubles) in shared memory when
+// it fits; taller matrices keep one L2-resident copy per CTA instead.
+bool cpqr_needs_xglobal(int64_t mrows, int64_t n, int num_sms) {
+    const int64_t G = std::min<int64_t>(n, num_sms);
+    const int cols = static_cast<int>((n + G - 1) / G);
+    return idk::cpqr_smem_bytes(static_cast<int>(mrows), cols) > 200 * 1024;
+}
 
 CpqrWs carve_cpqr(Carve& cv, int64_t mrows, int64_t n, int64_t k, int num_sms, const CpqrChoice& ch) {
     CpqrWs w;
+    if (!ch.resident && cpqr_needs_xglobal(mrows, n, num_sms)) {
+        w.has_xg = true;
+        w.xg = cv.take(sizeof(double) * static_cast<size_t>(std::min<int64_t>(n, num_sms)) *
+                       static_cast<size_t>(idk::cpqr_xglobal_ld(static_cast<int>(mrows))));
+    }
     w.pos = cv.take(sizeof(long long) * n);
     w.pivots = cv.take(sizeof(long long) * k);
     w.taus = cv.take(sizeof(double) * k);
@@ -185,7 +200,7 @@ int check_cpqr_fits(idk_context* h, int64_t mrows, int64_t n, const CpqrChoice& 
     if (ch.resident) return IDK_OK;
     const int64_t G = std::min<int64_t>(n, h->num_sms);
     const int cols = static_cast<int>((n + G - 1) / G);
-    if (idk::cpqr_smem_bytes(static_cast<int>(mrows), cols) > 200 * 1024)
+    if (idk::cpqr_smem_bytes(0, cols) > 200 * 1024)  // the per-column state (the reflector can live in L2)
         return set_err(h, IDK_ERR_INVALID_ARG,
                        "qr_column_pivoted: " + std::to_string(mrows) + " rows x " + std::to_string(n) +
                            " columns exceeds the persistent CPQR shared-memory budget");
@@ -202,7 +217,8 @@ cudaError_t run_cpqr(idk_context* h, const CpqrChoice& ch, double* W, int64_t mr
         return idk::cpqr_resident_launch(ch.plan, W, ldw, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv,
                                          taus, base + w.pub, reinterpret_cast<unsigned*>(base + w.barrier), h->stream);
     return idk::cpqr_launch(W, ldw, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
-                            reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream);
+                            reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream,
+                            w.has_xg ? reinterpret_cast<double*>(base + w.xg) : nullptr);
 }
 
 // CPQR(W) -> Z, C, cols; W is m' x n (ld m'), already resident and mutable.

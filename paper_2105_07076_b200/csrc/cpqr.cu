@@ -54,6 +54,8 @@ struct CpqrArgs {
     CpqrPub* pub;         // 2 * G (double-buffered by step parity)
     CpqrPub* pub2;        // G (exact tie pass)
     unsigned* barrier;    // zeroed before launch
+    double* xglobal;      // per-CTA reflector buffers (G x ldx) when m doubles do not fit in shared memory
+    int64_t ldx;
 };
 
 constexpr int kCpqrThreads = 256;
@@ -88,8 +90,10 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
     extern __shared__ __align__(16) double sm[];
     const int m = a.m;
     const int nc = a.cols_per_cta;
-    double* xv = sm;                       // m doubles: pivot column -> reflector
-    double* s_live = xv + ((m + 1) & ~1);  // nc
+    // m doubles: pivot column -> reflector; in shared memory, or for tall
+    // matrices (m > ~24k rows) this CTA's own L2-resident buffer
+    double* xv = a.xglobal ? a.xglobal + static_cast<int64_t>(blockIdx.x) * a.ldx : sm;
+    double* s_live = a.xglobal ? sm : xv + ((m + 1) & ~1);  // nc
     double* s_anchor = s_live + nc;        // nc
     long long* s_pos = reinterpret_cast<long long*>(s_anchor + nc);  // nc
 
@@ -107,8 +111,27 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
     const int64_t ldw = a.ldw;
     unsigned epoch = 0;
 
+    // Few columns per CTA (tall matrices): every warp of the CTA works on one
+    // column at a time (rows split over the whole block) instead of a warp per column.
+    const bool coop = myn < nwarps;
     // ---- initial squared norms (qr.cpp:56-62) ----
-    for (int lc = warp; lc < myn; lc += nwarps) {
+    if (coop) {
+        for (int lc = 0; lc < myn; ++lc) {
+            const double* col = W + (c0 + lc) * ldw;
+            double s = 0.0;
+            for (int i = tid; i < m; i += blockDim.x) {
+                const double v = ld_cg(col + i);
+                s += v * v;
+            }
+            s = block_sum(s, red_d);
+            if (tid == 0) {
+                s_live[lc] = s;
+                s_anchor[lc] = s;
+                s_pos[lc] = c0 + lc;
+            }
+        }
+    }
+    for (int lc = coop ? myn : warp; lc < myn; lc += nwarps) {
         const double* col = W + (c0 + lc) * ldw;
         double s = 0.0;
         for (int i = lane; i < m; i += 32) {
@@ -272,7 +295,43 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
         __syncthreads();
 
         // (2) trailing update + norm downdate (qr.cpp:93-106).
-        for (int lc = warp; lc < myn; lc += nwarps) {
+        if (coop) {  // one column at a time, rows over the whole block
+            for (int lc = 0; lc < myn; ++lc) {
+                if (s_pos[lc] <= s) continue;  // uniform across the block
+                double* col = W + (c0 + lc) * ldw + s;
+                double head;
+                if (tau != 0.0) {
+                    double d = 0.0;
+                    for (int i = 1 + tid; i < len; i += blockDim.x) d += xv[i] * ld_cg(col + i);
+                    d = block_sum(d, red_d);
+                    const double y0 = ld_cg(col);
+                    const double w = mul_rn(add_rn(y0, d), tau);
+                    head = sub_rn(y0, w);
+                    __syncthreads();  // every thread read y0 before it is overwritten
+                    if (tid == 0) st_cg(col, head);
+                    for (int i = 1 + tid; i < len; i += blockDim.x)
+                        st_cg(col + i, sub_rn(ld_cg(col + i), mul_rn(w, xv[i])));
+                } else {
+                    head = ld_cg(col);
+                }
+                double lv = sub_rn(s_live[lc], mul_rn(head, head));
+                if (lv < 0.0) lv = 0.0;
+                if (lv <= mul_rn(kRecompute, s_anchor[lc])) {
+                    __syncthreads();  // the updated rows are visible block-wide
+                    double f = 0.0;
+                    for (int i = 1 + tid; i < len; i += blockDim.x) {
+                        const double v = ld_cg(col + i);
+                        f += v * v;
+                    }
+                    f = block_sum(f, red_d);
+                    lv = f;
+                    if (tid == 0) s_anchor[lc] = f;
+                }
+                __syncthreads();
+                if (tid == 0) s_live[lc] = lv;
+            }
+        }
+        for (int lc = coop ? myn : warp; lc < myn; lc += nwarps) {
             if (s_pos[lc] <= s) continue;
             double* col = W + (c0 + lc) * ldw + s;
             double head;
@@ -374,15 +433,21 @@ size_t cpqr_smem_bytes(int m, int cols_per_cta) {
     return sizeof(double) * static_cast<size_t>(((m + 1) & ~1) + 3 * cols_per_cta);
 }
 
+// The reflector buffer moves to global memory (L2) when m doubles plus the
+// per-column state exceed the shared-memory budget; `xglobal` then needs G x
+// cpqr_xglobal_ld(m) doubles.
+int64_t cpqr_xglobal_ld(int m) { return (static_cast<int64_t>(m) + 31) & ~31LL; }
+
 // Host launcher.  `ws_pub` must hold 3*G CpqrPub, `barrier` one unsigned.
 cudaError_t cpqr_launch(double* W, int64_t ldw, int m, int64_t n, int k, long long* pos_out,
                         long long* pivots, double* taus, void* ws_pub, unsigned* barrier, int num_sms,
-                        int max_ctas, cudaStream_t stream) {
+                        int max_ctas, cudaStream_t stream, double* xglobal) {
     // Block-distribute columns: G CTAs, each at most one per SM (co-residency).
     int64_t G = std::min<int64_t>(n, static_cast<int64_t>(max_ctas > 0 ? max_ctas : num_sms));
     int cols = static_cast<int>((n + G - 1) / G);
     G = (n + cols - 1) / cols;
-    const size_t smem = cpqr_smem_bytes(m, cols);
+    const bool xg = xglobal && cpqr_smem_bytes(m, cols) > 200 * 1024;
+    const size_t smem = xg ? cpqr_smem_bytes(0, cols) : cpqr_smem_bytes(m, cols);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(cpqr_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -402,6 +467,8 @@ cudaError_t cpqr_launch(double* W, int64_t ldw, int m, int64_t n, int k, long lo
     args.pub = static_cast<CpqrPub*>(ws_pub);
     args.pub2 = static_cast<CpqrPub*>(ws_pub) + 2 * G;
     args.barrier = barrier;
+    args.xglobal = xg ? xglobal : nullptr;
+    args.ldx = cpqr_xglobal_ld(m);
     void* params[] = {&args};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_persistent_kernel), dim3(static_cast<unsigned>(G)),
                                        dim3(kCpqrThreads), params, smem, stream);

@@ -43,7 +43,8 @@ constexpr size_t kCpqrPubBytes = 32;
 size_t cpqr_smem_bytes(int m, int cols_per_cta);
 cudaError_t cpqr_launch(double* W, int64_t ldw, int m, int64_t n, int k, long long* pos_out, long long* pivots,
                         double* taus, void* ws_pub, unsigned* barrier, int num_sms, int max_ctas,
-                        cudaStream_t stream);
+                        cudaStream_t stream, double* xglobal = nullptr);
+int64_t cpqr_xglobal_ld(int m);
 cudaError_t cpqr_finish(const double* W, int64_t ldw, int m, int64_t n, int k, const long long* pos,
                         const long long* pivots, const double* taus, long long* perm, double* R, double* Q,
                         cudaStream_t stream);
