@@ -76,6 +76,14 @@ struct ResidentArgs {
     unsigned* barrier;        // debug: optional grid barrier before each exchange
     long long* trace;         // optional: %globaltimer at 8 phase marks per step, every CTA
     int push;                 // cluster: 1 = every CTA holds every candidate (push), 0 = headers only (pull)
+    // grid exchange layout: record stride in 64-bit words (>= kRecWords; a
+    // wider stride spreads the G polled records over more L2 lines / slices),
+    // copies of each published column (reader g reads copy g % copies, so the
+    // G simultaneous reads of the winner do not all hit the same lines), and
+    // the back-off of the record polls
+    int rec_stride;
+    int col_copies;
+    int poll_sleep_ns;
 };
 
 namespace {
@@ -796,6 +804,8 @@ cpqr_resident_kernel(ResidentArgs a) {
 
     // ---------------- grid exchange (tagged records in L2) ----------------
     auto slot_ptr = [&](int slot, int g) -> double* { return a.slots + (static_cast<size_t>(slot) * G + g) * gslot; };
+    // copy c of a slot (c = 0 is slot_ptr itself)
+    auto slot_copy = [&](double* base, int c) -> double* { return base + static_cast<size_t>(c) * 3 * G * gslot; };
 
     // Publish this CTA's candidate (local index winlc, position winpos) for the
     // exchange `tag` in `slot`: header + rows first..m-1, then the record.
@@ -807,28 +817,32 @@ cpqr_resident_kernel(ResidentArgs a) {
             partials(first, al, tl);
             double tu, be, sc;
             reflector(al, tl, m - first, tu, be, sc);
+            for (int cp = 0; cp < a.col_copies; ++cp) {
+                double* dc = slot_copy(dst, cp);
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int i = l0 + q + S * r;
-                if (i >= first && i < m) dst[kHdr + i - first] = yr[r];
-            }
-            if (q == 0) {
-                dst[0] = __longlong_as_double(c0 + winlc);
-                dst[1] = tu;
-                dst[2] = be;
-                dst[3] = sc;
+                for (int r = 0; r < R; ++r) {
+                    const int i = l0 + q + S * r;
+                    if (i >= first && i < m) dc[kHdr + i - first] = yr[r];
+                }
+                if (q == 0) {
+                    dc[0] = __longlong_as_double(c0 + winlc);
+                    dc[1] = tu;
+                    dc[2] = be;
+                    dc[3] = sc;
+                }
             }
         }
         if (have) {  // shared-memory rows of the candidate, copied by everyone
             const double* cr = rows + static_cast<size_t>(winlc) * lds;
-            for (int i = first + tid; i < l0; i += T) dst[kHdr + i - first] = cr[i];
+            for (int cp = 0; cp < a.col_copies; ++cp)
+                for (int i = first + tid; i < l0; i += T) slot_copy(dst, cp)[kHdr + i - first] = cr[i];
         }
         __syncthreads();
         if (tid == 0) {
             const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
             __threadfence();  // slot data before the tagged record (release)
             const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
-            unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * kRecWords;
+            unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * a.rec_stride;
             st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
             st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
         }
@@ -837,13 +851,14 @@ cpqr_resident_kernel(ResidentArgs a) {
     // Record of CTA g for exchange `tag`: {vmax, pos}; spins until all three
     // words carry the tag.
     auto read_rec = [&](int slot, int g, unsigned tag, double& vmax, unsigned& pos) {
-        const unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + g) * kRecWords;
+        const unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + g) * a.rec_stride;
         unsigned long long x0, x1, x2, x3;
         for (;;) {
             ld_relaxed_v2(rp, x0, x1);
             ld_relaxed_v2(rp + 2, x2, x3);
             if (static_cast<unsigned>(x0) == tag && static_cast<unsigned>(x1) == tag && static_cast<unsigned>(x2) == tag)
                 break;
+            if (a.poll_sleep_ns > 0) __nanosleep(a.poll_sleep_ns);
         }
         vmax = __longlong_as_double(static_cast<long long>(((x0 >> 32) << 32) | (x1 >> 32)));
         pos = static_cast<unsigned>(x2 >> 32);
@@ -938,7 +953,7 @@ cpqr_resident_kernel(ResidentArgs a) {
         }
         trace(step, 5);
         // All threads: header + winner's column (one round trip), scaled into xbuf by absolute row.
-        const double* src = slot_ptr(slot, gsel);
+        const double* src = slot_copy(slot_ptr(slot, gsel), me % a.col_copies);
         const double h0 = __ldcg(src);
         const double tu = __ldcg(src + 1);
         const double be = __ldcg(src + 2);
@@ -990,19 +1005,20 @@ cpqr_resident_kernel(ResidentArgs a) {
                 double al = 0.0, tl = 0.0;
                 for (int i = first + lane; i < m; i += 32) {
                     const double y = fma(-ww, xa[i], i < l0 ? wrow[i] : xscr[i]);  // == the group's own axpy
-                    dst[kHdr + i - first] = y;
+                    for (int cp = 0; cp < a.col_copies; ++cp) slot_copy(dst, cp)[kHdr + i - first] = y;
                     if (i == first) al = y;
                     else tl = fma(y, y, tl);
                 }
                 al = __shfl_sync(kFull, al, 0);
                 tl = warp_sum(tl);
-                if (lane == 0) {
+                if (lane < a.col_copies) {
                     double tu, be, sc;
                     reflector(al, tl, m - first, tu, be, sc);
-                    dst[0] = __longlong_as_double(c0 + winlc);
-                    dst[1] = tu;
-                    dst[2] = be;
-                    dst[3] = sc;
+                    double* dc = slot_copy(dst, lane);
+                    dc[0] = __longlong_as_double(c0 + winlc);
+                    dc[1] = tu;
+                    dc[2] = be;
+                    dc[3] = sc;
                 }
             }
             __threadfence();  // slot data before the tagged record (release)
@@ -1010,7 +1026,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             if (lane == 0) {
                 const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
                 const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
-                unsigned long long* rp = a.rec + (static_cast<size_t>(parity) * G + me) * kRecWords;
+                unsigned long long* rp = a.rec + (static_cast<size_t>(parity) * G + me) * a.rec_stride;
                 st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
                 st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
             }
@@ -1308,11 +1324,26 @@ long long* g_trace = nullptr;  // debug: set by idk_debug_cpqr_trace
 
 void cpqr_resident_set_trace(long long* p) { g_trace = p; }
 
+namespace {
+// grid-exchange layout knobs (tools/exp_grid_exchange.py; defaults = the measured best,
+// profiles/grid_exchange_r02.txt: 4 column copies take cfg4 8.39 -> 7.53 us per step,
+// cfg5 8.26 -> 7.50; a wider record stride or poll back-off gains nothing on top)
+int env_int(const char* name, int dflt, int lo, int hi) {
+    const char* v = getenv(name);
+    if (!v) return dflt;
+    const int x = atoi(v);
+    return x < lo ? lo : (x > hi ? hi : x);
+}
+int rec_stride() { return env_int("IDK_REC_STRIDE", kRecWords, kRecWords, 64); }
+int col_copies() { return env_int("IDK_COL_COPIES", 4, 1, 8); }
+int poll_sleep_ns() { return env_int("IDK_POLL_SLEEP", 0, 0, 1000); }
+}  // namespace
+
 size_t cpqr_resident_exchange_bytes(const ResidentPlan& p, int m) {
     if (!p.ok || p.cluster) return 0;
     const size_t G = static_cast<size_t>(p.G);
     const size_t slot_len = kHdr + static_cast<size_t>((m + 1) & ~1);
-    return sizeof(unsigned long long) * kRecWords * 3 * G + sizeof(double) * 3 * G * slot_len + 256;
+    return sizeof(unsigned long long) * 64 * 3 * G + sizeof(double) * 8 * 3 * G * slot_len + 256;
 }
 
 cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, int m, int64_t n, int k,
@@ -1332,8 +1363,11 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     a.taus = taus;
     const size_t G = static_cast<size_t>(p.G);
     char* e = static_cast<char*>(exch);
+    a.rec_stride = p.cluster ? kRecWords : rec_stride();
+    a.col_copies = p.cluster ? 1 : col_copies();
+    a.poll_sleep_ns = p.cluster ? 0 : poll_sleep_ns();
     a.rec = reinterpret_cast<unsigned long long*>(e);
-    a.slots = reinterpret_cast<double*>(e + sizeof(unsigned long long) * kRecWords * 3 * G);
+    a.slots = reinterpret_cast<double*>(e + sizeof(unsigned long long) * a.rec_stride * 3 * G);
     a.trace = g_trace;
     a.push = p.push ? 1 : 0;
     void* args[] = {&a};
@@ -1362,7 +1396,7 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
     if (err != cudaSuccess) return err;
     // records start untagged (tags are 1..k, so stale records never match)
-    err = cudaMemsetAsync(exch, 0, sizeof(unsigned long long) * kRecWords * 3 * G, stream);
+    err = cudaMemsetAsync(exch, 0, sizeof(unsigned long long) * a.rec_stride * 3 * G, stream);
     if (err != cudaSuccess) return err;
     a.barrier = nullptr;
     if (getenv("IDK_DEBUG_GRID_BARRIER")) {

@@ -57,13 +57,20 @@ print(f"step (cta0): mean {tot.mean():.0f} ns  first {tot[0]:.0f}  last {tot[-1]
 if t[:, :steps, 7].max() > 0:
     d = t[:, :steps, 7] - t[:, :steps, 2]
     print(f"{'(tid0 deferred axpy)':24s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
-if t[:, :steps, 8].max() > 0:  # cluster publish path of the winner warp (marks 2 -> 8..12 -> 3)
-    pw = [("winner rows staged", 2, 8), ("pending update + norm", 8, 9), ("reflector scalars", 9, 10),
-          ("scaled v + header", 10, 11), ("fence.proxy.async", 11, 12), ("bulk pushes issued", 12, 3)]
-    for nm, a0, a1 in pw:
+def recorded(*marks):
+    """A phase is printed only when every CTA recorded both of its marks in every
+    step (grid mode never records the cluster-only marks 9-12)."""
+    return all((t[:, :steps, mk] > 0).all() for mk in marks)
+
+
+# cluster publish path of the winner warp (marks 2 -> 8..12 -> 3)
+pw = [("winner rows staged", 2, 8), ("pending update + norm", 8, 9), ("reflector scalars", 9, 10),
+      ("scaled v + header", 10, 11), ("fence.proxy.async", 11, 12), ("bulk pushes issued", 12, 3)]
+for nm, a0, a1 in pw:
+    if recorded(a0, a1):
         d = t[:, :steps, a1] - t[:, :steps, a0]
         print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
-if t[:, :steps, 13].max() > 0:  # grid select: records -> vmax -> winner (before the tie pass) -> done
+if recorded(4, 13, 14, 5):  # grid select: records -> vmax -> winner (before the tie pass) -> done
     for nm, a0, a1 in [("  records -> vmax", 4, 13), ("  vmax -> winner", 13, 14), ("  tie pass / rest", 14, 5)]:
         d = t[:, :steps, a1] - t[:, :steps, a0]
         print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
