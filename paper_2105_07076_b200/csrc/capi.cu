@@ -751,16 +751,7 @@ int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t
         if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
         status = reinterpret_cast<int*>(h->ws + sofs);
     }
-    // throughput kernels: batched_duo (two matrices per SM) unless IDK_BATCHED_KERNEL=fast selects
-    // batched_fast (one matrix per SM, 64 register rows, TMA prefetch)
-    const char* bk = getenv("IDK_BATCHED_KERNEL");
-    const bool duo = fast && !(bk && std::strcmp(bk, "fast") == 0) &&
-                     idk::batched_duo_ok(d_a, lda, stride, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k));
-    if (duo)
-        IDK_CUDA(idk::batched_id_duo(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n),
-                                     static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
-                                     h->num_sms, h->stream));
-    else if (fast)
+    if (fast)
         IDK_CUDA(idk::batched_id_fast(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n),
                                       static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
                                       h->num_sms, h->stream));
