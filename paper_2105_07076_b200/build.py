@@ -39,8 +39,13 @@ def up_to_date(target, deps):
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    objdir = os.path.join(PKG, "build")
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+    """trace=True: a separate debug library (libidkit_b200_trace.so) whose
+    resident CPQR records per-step phase marks for tools/trace_cpqr.py
+    (-DIDK_CPQR_TRACE; the product library carries no trace code)."""
+    objdir = os.path.join(PKG, "build_trace" if trace else "build")
+    lib = os.path.join(PKG, "libidkit_b200_trace.so") if trace else LIB
+    flags = FLAGS + (["-DIDK_CPQR_TRACE"] if trace else [])
     os.makedirs(objdir, exist_ok=True)
     objs, jobs = [], []
     hdrs = headers()
@@ -49,7 +54,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
         if not force and up_to_date(obj, [src] + hdrs):
             continue
-        cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + ARCH + flags + ["-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)
@@ -57,12 +62,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
     # translation units compile independently: one nvcc per core
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
         list(pool.map(lambda c: subprocess.run(c, check=True), jobs))
-    if force or not up_to_date(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+    if force or not up_to_date(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
-    print(LIB)
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, trace="--trace" in sys.argv))

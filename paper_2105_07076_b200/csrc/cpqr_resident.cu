@@ -57,6 +57,11 @@ namespace idk {
 constexpr int kHdr = 4;
 constexpr int kCHdr = 6;  // cluster slot header: col, tau, beta, scale, vmax, pos
 constexpr int kRecWords = 4;  // vmax hi | vmax lo | pos | pad
+// Copies of each published grid-mode column: after the records every CTA reads
+// the winner's column at the same moment, and with one copy all G readers hit
+// the same ~17 L2 lines; reader g reads copy g % kColCopies
+// (profiles/grid_exchange_r02.txt: cfg4 8.39 -> 7.53 us per step).
+constexpr int kColCopies = 4;
 
 struct ResidentArgs {
     double* W;
@@ -76,14 +81,6 @@ struct ResidentArgs {
     unsigned* barrier;        // debug: optional grid barrier before each exchange
     long long* trace;         // optional: %globaltimer at 8 phase marks per step, every CTA
     int push;                 // cluster: 1 = every CTA holds every candidate (push), 0 = headers only (pull)
-    // grid exchange layout: record stride in 64-bit words (>= kRecWords; a
-    // wider stride spreads the G polled records over more L2 lines / slices),
-    // copies of each published column (reader g reads copy g % copies, so the
-    // G simultaneous reads of the winner do not all hit the same lines), and
-    // the back-off of the record polls
-    int rec_stride;
-    int col_copies;
-    int poll_sleep_ns;
 };
 
 namespace {
@@ -289,17 +286,27 @@ cpqr_resident_kernel(ResidentArgs a) {
     const int gbase = lane & ~(S - 1);
     constexpr unsigned kFull = 0xffffffffu;
 
+    // phase marks (tools/trace_cpqr.py) exist only in builds with -DIDK_CPQR_TRACE:
+    // the checks cost code size in the step loop, which the serial phases feel
     auto trace_by = [&](bool who, int s, int ph) {
+#ifdef IDK_CPQR_TRACE
         if (a.trace != nullptr && who && s >= 0)
             a.trace[(static_cast<size_t>(me) * (a.k + 1) + s) * 16 + ph] = globaltimer();
+#else
+        (void)who;
+        (void)s;
+        (void)ph;
+#endif
     };
     auto trace = [&](int s, int ph) { trace_by(tid == 0, s, ph); };
 
+#ifdef IDK_CPQR_TRACE
     if (a.trace != nullptr && tid == 0) {  // debug: which SM this CTA runs on (slot 15 of row k)
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[(static_cast<size_t>(me) * (a.k + 1) + a.k) * 16 + 15] = smid;
     }
+#endif
     for (int i = tid; i < 3 * xlen; i += T) xbuf[i] = 0.0;
     if constexpr (kCluster) {
         const int zn = push ? 3 * G * cslot : 3 * cslot + 3 * G * kCHdr;
@@ -817,7 +824,8 @@ cpqr_resident_kernel(ResidentArgs a) {
             partials(first, al, tl);
             double tu, be, sc;
             reflector(al, tl, m - first, tu, be, sc);
-            for (int cp = 0; cp < a.col_copies; ++cp) {
+#pragma unroll
+            for (int cp = 0; cp < kColCopies; ++cp) {
                 double* dc = slot_copy(dst, cp);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -834,7 +842,7 @@ cpqr_resident_kernel(ResidentArgs a) {
         }
         if (have) {  // shared-memory rows of the candidate, copied by everyone
             const double* cr = rows + static_cast<size_t>(winlc) * lds;
-            for (int cp = 0; cp < a.col_copies; ++cp)
+            for (int cp = 0; cp < kColCopies; ++cp)
                 for (int i = first + tid; i < l0; i += T) slot_copy(dst, cp)[kHdr + i - first] = cr[i];
         }
         __syncthreads();
@@ -842,7 +850,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
             __threadfence();  // slot data before the tagged record (release)
             const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
-            unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * a.rec_stride;
+            unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * kRecWords;
             st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
             st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
         }
@@ -851,14 +859,13 @@ cpqr_resident_kernel(ResidentArgs a) {
     // Record of CTA g for exchange `tag`: {vmax, pos}; spins until all three
     // words carry the tag.
     auto read_rec = [&](int slot, int g, unsigned tag, double& vmax, unsigned& pos) {
-        const unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + g) * a.rec_stride;
+        const unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + g) * kRecWords;
         unsigned long long x0, x1, x2, x3;
         for (;;) {
             ld_relaxed_v2(rp, x0, x1);
             ld_relaxed_v2(rp + 2, x2, x3);
             if (static_cast<unsigned>(x0) == tag && static_cast<unsigned>(x1) == tag && static_cast<unsigned>(x2) == tag)
                 break;
-            if (a.poll_sleep_ns > 0) __nanosleep(a.poll_sleep_ns);
         }
         vmax = __longlong_as_double(static_cast<long long>(((x0 >> 32) << 32) | (x1 >> 32)));
         pos = static_cast<unsigned>(x2 >> 32);
@@ -953,7 +960,7 @@ cpqr_resident_kernel(ResidentArgs a) {
         }
         trace(step, 5);
         // All threads: header + winner's column (one round trip), scaled into xbuf by absolute row.
-        const double* src = slot_copy(slot_ptr(slot, gsel), me % a.col_copies);
+        const double* src = slot_copy(slot_ptr(slot, gsel), me % kColCopies);
         const double h0 = __ldcg(src);
         const double tu = __ldcg(src + 1);
         const double be = __ldcg(src + 2);
@@ -1005,13 +1012,14 @@ cpqr_resident_kernel(ResidentArgs a) {
                 double al = 0.0, tl = 0.0;
                 for (int i = first + lane; i < m; i += 32) {
                     const double y = fma(-ww, xa[i], i < l0 ? wrow[i] : xscr[i]);  // == the group's own axpy
-                    for (int cp = 0; cp < a.col_copies; ++cp) slot_copy(dst, cp)[kHdr + i - first] = y;
+#pragma unroll
+                    for (int cp = 0; cp < kColCopies; ++cp) slot_copy(dst, cp)[kHdr + i - first] = y;
                     if (i == first) al = y;
                     else tl = fma(y, y, tl);
                 }
                 al = __shfl_sync(kFull, al, 0);
                 tl = warp_sum(tl);
-                if (lane < a.col_copies) {
+                if (lane < kColCopies) {
                     double tu, be, sc;
                     reflector(al, tl, m - first, tu, be, sc);
                     double* dc = slot_copy(dst, lane);
@@ -1026,7 +1034,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             if (lane == 0) {
                 const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
                 const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
-                unsigned long long* rp = a.rec + (static_cast<size_t>(parity) * G + me) * a.rec_stride;
+                unsigned long long* rp = a.rec + (static_cast<size_t>(parity) * G + me) * kRecWords;
                 st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
                 st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
             }
@@ -1324,26 +1332,11 @@ long long* g_trace = nullptr;  // debug: set by idk_debug_cpqr_trace
 
 void cpqr_resident_set_trace(long long* p) { g_trace = p; }
 
-namespace {
-// grid-exchange layout knobs (tools/exp_grid_exchange.py; defaults = the measured best,
-// profiles/grid_exchange_r02.txt: 4 column copies take cfg4 8.39 -> 7.53 us per step,
-// cfg5 8.26 -> 7.50; a wider record stride or poll back-off gains nothing on top)
-int env_int(const char* name, int dflt, int lo, int hi) {
-    const char* v = getenv(name);
-    if (!v) return dflt;
-    const int x = atoi(v);
-    return x < lo ? lo : (x > hi ? hi : x);
-}
-int rec_stride() { return env_int("IDK_REC_STRIDE", kRecWords, kRecWords, 64); }
-int col_copies() { return env_int("IDK_COL_COPIES", 4, 1, 8); }
-int poll_sleep_ns() { return env_int("IDK_POLL_SLEEP", 0, 0, 1000); }
-}  // namespace
-
 size_t cpqr_resident_exchange_bytes(const ResidentPlan& p, int m) {
     if (!p.ok || p.cluster) return 0;
     const size_t G = static_cast<size_t>(p.G);
     const size_t slot_len = kHdr + static_cast<size_t>((m + 1) & ~1);
-    return sizeof(unsigned long long) * 64 * 3 * G + sizeof(double) * 8 * 3 * G * slot_len + 256;
+    return sizeof(unsigned long long) * kRecWords * 3 * G + sizeof(double) * kColCopies * 3 * G * slot_len + 256;
 }
 
 cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, int m, int64_t n, int k,
@@ -1363,11 +1356,8 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     a.taus = taus;
     const size_t G = static_cast<size_t>(p.G);
     char* e = static_cast<char*>(exch);
-    a.rec_stride = p.cluster ? kRecWords : rec_stride();
-    a.col_copies = p.cluster ? 1 : col_copies();
-    a.poll_sleep_ns = p.cluster ? 0 : poll_sleep_ns();
     a.rec = reinterpret_cast<unsigned long long*>(e);
-    a.slots = reinterpret_cast<double*>(e + sizeof(unsigned long long) * a.rec_stride * 3 * G);
+    a.slots = reinterpret_cast<double*>(e + sizeof(unsigned long long) * kRecWords * 3 * G);
     a.trace = g_trace;
     a.push = p.push ? 1 : 0;
     void* args[] = {&a};
@@ -1396,7 +1386,7 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem));
     if (err != cudaSuccess) return err;
     // records start untagged (tags are 1..k, so stale records never match)
-    err = cudaMemsetAsync(exch, 0, sizeof(unsigned long long) * a.rec_stride * 3 * G, stream);
+    err = cudaMemsetAsync(exch, 0, sizeof(unsigned long long) * kRecWords * 3 * G, stream);
     if (err != cudaSuccess) return err;
     a.barrier = nullptr;
     if (getenv("IDK_DEBUG_GRID_BARRIER")) {

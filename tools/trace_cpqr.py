@@ -1,5 +1,7 @@
 """Per-phase breakdown of the resident CPQR kernel from %globaltimer marks of
-every CTA: python tools/trace_cpqr.py cfg2 [mode]
+every CTA.  The marks exist only in the debug library:
+  python -m paper_2105_07076_b200.build --trace
+  IDK_LIB_PATH=paper_2105_07076_b200/libidkit_b200_trace.so python tools/trace_cpqr.py cfg2 [mode]
 
 Marks per step s: 0 top, 1 trailing update (cluster: dot + downdate) done,
 2 CTA argmax done, 3 candidate + record published (cluster: by the publishing
