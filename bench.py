@@ -258,7 +258,11 @@ def run_ours(args):
         a = (a[begin:end, :] if tall else a[:, begin:end]).t().contiguous().t()
     nccl_path = use_sharded and backend == "nccl"  # the C-ABI entry idk_id_sharded over its own NCCL communicator
     if nccl_path:
-        sharded.nccl_setup(local)
+        try:
+            sharded.nccl_setup(local)
+        except Exception as exc:  # noqa: BLE001 -- keep the run alive on the torch.distributed path
+            print(f"bench.py: C-ABI NCCL setup failed ({exc}); sharded path via torch.distributed", file=sys.stderr)
+            nccl_path = False
     torch.cuda.empty_cache()
     ctx = idk.context(local)
     ctx.set_profiling(False)  # per-stage events cost ~35% with 8 IDs in flight: a separate pass records them

@@ -220,13 +220,29 @@ IDK_API int idk_comm_destroy(idk_handle h);
  * Z for the local columns into d_z_local (k x (end-begin), ld = k) -> the
  * pivot columns this rank owns gathered into d_c and one grouped
  * ncclBroadcast per column from its owner, so C (m x k, ld = m) is complete
- * and bit-exact on every rank (optional).  d_cols (k) = global column ids of
+ * and bit-exact on every rank (optional).  Peer mode (default when every rank
+ * can map the others' memory by CUDA IPC; IDK_SHARD_P2P=0 turns it off): the
+ * all-gather is fused into the sketch -- its split-K reduction stores each
+ * finished Y element into every rank's Y buffer over NVLink
+ * (idk_sketch_fanout), bracketed by two stream-ordered one-int barriers.  d_cols (k) = global column ids of
  * M (row ids of A for the dual).  Results equal idk_sketch_rid's on the
- * unsharded matrix bit for bit.  Without a communicator the call runs as one
- * rank. */
+ * unsharded matrix bit for bit (the split-K count is the unsharded one).
+ * Without a communicator the call runs as one rank. */
 IDK_API int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, int64_t lda, int a_transposed,
                            int64_t k, int64_t p, uint64_t seed, int omega_mode, const double* d_omega,
                            int64_t* d_cols, double* d_z_local, double* d_c);
+
+/* The sharded sketch with its all-gather fused in (what idk_id_sharded runs in
+ * peer mode, where d_dst are the ranks' Y buffers mapped over NVLink by CUDA
+ * IPC): Y_block (l x n) = Omega (l x m, ld = l) * M_block, M_block = A
+ * (m x n, lda) or the transpose of the stored n x m block (a_transposed), and
+ * the split-K reduction stores every finished element to all ndst (<= 8)
+ * destinations d_dst[g] (ld = ldy).  The split-K count is the one of an
+ * n_total-column sketch, so the block is bit-identical to the same columns of
+ * idk_sketch on the whole matrix.  d_dst is a host array of device pointers. */
+IDK_API int idk_sketch_fanout(idk_handle h, const double* d_omega, int64_t l, const double* d_a, int64_t m, int64_t n,
+                              int64_t lda, int a_transposed, double* const* d_dst, int ndst, int64_t ldy,
+                              int64_t n_total);
 
 /* Concurrent entry for a stream of independent IDs (serving): `count` m x n
  * matrices d_a[i] (device, lda), results into d_cols[i], d_z[i] (k * max(m, n))

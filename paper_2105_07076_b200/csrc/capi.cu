@@ -66,6 +66,13 @@ struct idk_context {
     idk::ncclComm_t nccl_comm = nullptr;
     bool nccl_owned = false;
     int nranks = 1, rank = 0;
+    // peer mode of idk_id_sharded: every rank's Y buffer mapped into every other
+    // rank (CUDA IPC over NVLink); the sketch writes its block straight into all of them
+    double* ybuf = nullptr;  // this rank's Y (its own cudaMalloc: IPC exports whole allocations)
+    size_t ybuf_cap = 0;
+    double* peer_y[idk::kFanMax] = {};
+    int* d_flag = nullptr;   // 1-int scratch of the stream-ordered barrier / agreement
+    int p2p_state = 0;       // 0 untried, 1 on, -1 off (IPC unavailable: the NCCL all-gather runs)
 };
 
 namespace {
@@ -624,6 +631,10 @@ int idk_destroy(idk_handle h) {
     for (cudaEvent_t e : h->ev_io) cudaEventDestroy(e);
     if (h->s_in) cudaStreamDestroy(h->s_in);
     if (h->s_out) cudaStreamDestroy(h->s_out);
+    for (int g = 0; g < idk::kFanMax; ++g)
+        if (h->peer_y[g] && h->peer_y[g] != h->ybuf) cudaIpcCloseMemHandle(h->peer_y[g]);
+    if (h->ybuf) cudaFree(h->ybuf);
+    if (h->d_flag) cudaFree(h->d_flag);
     if (h->nccl_comm && h->nccl_owned) {
         if (const idk::NcclApi* api = idk::nccl_api(nullptr)) api->CommDestroy(h->nccl_comm);
     }
@@ -1610,6 +1621,106 @@ int idk_comm_destroy(idk_handle h) {
     return IDK_OK;
 }
 
+int idk_sketch_fanout(idk_handle h, const double* d_omega, int64_t l, const double* d_a, int64_t m, int64_t n,
+                      int64_t lda, int a_transposed, double* const* d_dst, int ndst, int64_t ldy, int64_t n_total) {
+    if (!h) return IDK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    if (l <= 0 || m <= 0 || n < 0 || l > INT_MAX || n_total < n || ndst < 1 || ndst > idk::kFanMax || !d_dst ||
+        ldy < l || lda < (a_transposed ? n : m))
+        return set_err(h, IDK_ERR_INVALID_ARG, "sketch_fanout: bad arguments");
+    if (n == 0) return IDK_OK;
+    idk::FanOut f;
+    f.count = ndst;
+    for (int g = 0; g < ndst; ++g) f.y[g] = d_dst[g];
+    const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(l), n_total, m, h->num_sms);
+    int rc;
+    if (splits > 1 && (rc = ensure(h, &h->ws, &h->ws_cap, sizeof(double) * ldy * n * splits))) return rc;
+    IDK_CUDA(idk::sketch_gemm_fanout(d_omega, l, d_a, lda, a_transposed != 0, f, ldy, static_cast<int>(l), n, m, splits,
+                                     reinterpret_cast<double*>(h->ws), h->stream));
+    h->launches += 2;
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    return IDK_OK;
+}
+
+// Peer mode setup (collective over the communicator): (re)allocate this rank's
+// Y buffer, all-gather the CUDA IPC handles with NCCL, open the peers'
+// buffers, and agree (NCCL min) that every rank succeeded -- otherwise every
+// rank falls back to the NCCL all-gather together.
+static int peer_setup(idk_handle h, const idk::NcclApi* api, size_t bytes) {
+    const int G = h->nranks;
+    if (h->p2p_state == -1) return IDK_OK;
+    if (h->p2p_state == 1 && bytes <= h->ybuf_cap) return IDK_OK;
+    const char* env = getenv("IDK_SHARD_P2P");
+    if (G > idk::kFanMax || (env && atoi(env) == 0)) {
+        h->p2p_state = -1;
+        return IDK_OK;
+    }
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    for (int g = 0; g < idk::kFanMax; ++g) {
+        if (h->peer_y[g] && h->peer_y[g] != h->ybuf) cudaIpcCloseMemHandle(h->peer_y[g]);
+        h->peer_y[g] = nullptr;
+    }
+    if (h->ybuf) cudaFree(h->ybuf);
+    h->ybuf = nullptr;
+    h->ybuf_cap = 0;
+    if (!h->d_flag) IDK_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->d_flag), 2 * sizeof(int)));
+    int ok = 1;
+    cudaIpcMemHandle_t mine;
+    std::memset(&mine, 0, sizeof(mine));
+    if (cudaMalloc(reinterpret_cast<void**>(&h->ybuf), bytes) != cudaSuccess ||
+        cudaIpcGetMemHandle(&mine, h->ybuf) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+    }
+    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(G));
+    char* d_h = nullptr;
+    IDK_CUDA(cudaMalloc(reinterpret_cast<void**>(&d_h), sizeof(cudaIpcMemHandle_t) * (G + 1)));
+    IDK_CUDA(cudaMemcpyAsync(d_h + sizeof(cudaIpcMemHandle_t) * h->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice,
+                             h->stream));
+    idk::ncclResult_t r = api->AllGather(d_h + sizeof(cudaIpcMemHandle_t) * h->rank, d_h, sizeof(cudaIpcMemHandle_t),
+                                         idk::kNcclUint8, h->nccl_comm, h->stream);
+    if (r != 0) {
+        cudaFree(d_h);
+        return set_err(h, IDK_ERR_NCCL, std::string("ncclAllGather (IPC handles): ") + api->GetErrorString(r));
+    }
+    IDK_CUDA(cudaMemcpyAsync(all.data(), d_h, sizeof(cudaIpcMemHandle_t) * G, cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    cudaFree(d_h);
+    for (int g = 0; g < G && ok; ++g) {
+        if (g == h->rank) {
+            h->peer_y[g] = h->ybuf;
+            continue;
+        }
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[g], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+        } else {
+            h->peer_y[g] = static_cast<double*>(p);
+        }
+    }
+    // every rank must take the same path
+    IDK_CUDA(cudaMemcpyAsync(h->d_flag, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    r = api->AllReduce(h->d_flag, h->d_flag, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
+    if (r != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllReduce: ") + api->GetErrorString(r));
+    int all_ok = 0;
+    IDK_CUDA(cudaMemcpyAsync(&all_ok, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    if (!all_ok) {
+        for (int g = 0; g < idk::kFanMax; ++g) {
+            if (h->peer_y[g] && h->peer_y[g] != h->ybuf) cudaIpcCloseMemHandle(h->peer_y[g]);
+            h->peer_y[g] = nullptr;
+        }
+        if (h->ybuf) cudaFree(h->ybuf);
+        h->ybuf = nullptr;
+        h->p2p_state = -1;
+        return IDK_OK;
+    }
+    h->ybuf_cap = bytes;
+    h->p2p_state = 1;
+    return IDK_OK;
+}
+
 int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, int64_t lda, int a_transposed,
                    int64_t k, int64_t p, uint64_t seed, int omega_mode, const double* d_omega, int64_t* d_cols,
                    double* d_z_local, double* d_c) {
@@ -1637,10 +1748,15 @@ int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, 
     const int64_t l = k + p;
     const CpqrChoice ch = choose_cpqr(h, l, n, k);
     if ((rc = check_cpqr_fits(h, l, n, ch))) return rc;
-    const int splits = nr > 0 ? idk::sketch_gemm_pick_splits(static_cast<int>(l), nr, m, h->num_sms) : 1;
+    // the split-K count of the unsharded sketch: every element of Y is summed in
+    // the same order as on one GPU, so the sharded result is bit-identical
+    const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(l), n, m, h->num_sms);
+    const size_t ybytes = sizeof(double) * l * w * G;  // rank q's block at column q*w
+    if (G > 1 && (rc = peer_setup(h, api, ybytes))) return rc;
+    const bool p2p = G > 1 && h->p2p_state == 1;
     Carve cv;
     const size_t oofs = omega_mode == IDK_OMEGA_VERBATIM ? 0 : cv.take(sizeof(double) * l * m);
-    const size_t yofs = cv.take(sizeof(double) * l * w * G);  // rank q's block at column q*w: one in-place all-gather
+    const size_t yofs = p2p ? 0 : cv.take(ybytes);  // NCCL mode: one in-place all-gather
     const size_t pofs = splits > 1 ? cv.take(sizeof(double) * l * nr * splits) : 0;
     const CpqrWs ws = carve_cpqr(cv, l, n, k, h->num_sms, ch);
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
@@ -1658,13 +1774,36 @@ int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, 
         h->launches += omega_mode == IDK_OMEGA_PHILOX ? 1 : 0;
         omega = om;
     }
-    double* Y = reinterpret_cast<double*>(h->ws + yofs);
-    if (nr > 0) {  // this rank's columns of Y = Omega M, straight into its slot of the gathered Y
+    double* Y = p2p ? h->ybuf : reinterpret_cast<double*>(h->ws + yofs);
+    if (p2p) {
+        // the all-gather fused into the sketch: the split-K reduction stores this
+        // rank's block into every rank's Y over NVLink, then a stream-ordered
+        // barrier (a one-int NCCL all-reduce) tells each rank its Y is complete.  A
+        // first barrier keeps this call's stores out of a peer's Y until that
+        // peer's previous call (whose CPQR factors its Y in place) is done.
+        const idk::ncclResult_t pr =
+            api->AllReduce(h->d_flag, h->d_flag + 1, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
+        if (pr != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllReduce (barrier): ") + api->GetErrorString(pr));
+        if (nr > 0) {
+            idk::FanOut f;
+            f.count = G;
+            f.y[0] = Y + b * l;
+            for (int g = 0, t = 1; g < G; ++g)
+                if (g != r) f.y[t++] = h->peer_y[g] + b * l;
+            IDK_CUDA(idk::sketch_gemm_fanout(omega, l, d_a_local, lda, trans, f, l, static_cast<int>(l), nr, m, splits,
+                                             splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr,
+                                             h->stream));
+            h->launches += 2;
+        }
+        const idk::ncclResult_t br =
+            api->AllReduce(h->d_flag, h->d_flag + 1, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
+        if (br != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllReduce (barrier): ") + api->GetErrorString(br));
+    } else if (nr > 0) {  // this rank's columns of Y = Omega M, straight into its slot of the gathered Y
         IDK_CUDA(idk::sketch_gemm(omega, l, d_a_local, lda, trans, Y + b * l, l, static_cast<int>(l), nr, m, splits,
                                   splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr, h->stream));
         h->launches += splits > 1 ? 2 : 1;
     }
-    if (G > 1) {
+    if (G > 1 && !p2p) {
         const idk::ncclResult_t nr_ = api->AllGather(Y + static_cast<int64_t>(r) * w * l, Y, static_cast<size_t>(w * l),
                                                     idk::kNcclFloat64, h->nccl_comm, h->stream);
         if (nr_ != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllGather: ") + api->GetErrorString(nr_));

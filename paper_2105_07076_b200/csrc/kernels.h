@@ -15,6 +15,14 @@ struct GemmGroup {  // grouped sketch members (kernel parameter, by value)
     const double* b[kGemmGroupMax];
     double* y[kGemmGroupMax];
 };
+constexpr int kFanMax = 8;
+struct FanOut {  // destinations of a sharded sketch block (kernel parameter, by value)
+    double* y[kFanMax];
+    int count = 0;
+};
+cudaError_t sketch_gemm_fanout(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans, const FanOut& f,
+                               int64_t ldc, int M, int64_t N, int64_t K, int splits, double* partial,
+                               cudaStream_t stream);
 struct GroupSeeds {
     uint64_t s[kGemmGroupMax];
 };

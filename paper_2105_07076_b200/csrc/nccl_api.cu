@@ -42,6 +42,7 @@ const NcclApi* nccl_api(std::string* err) {
         all &= bind(lib, "ncclCommUserRank", &api.CommUserRank, &missing);
         all &= bind(lib, "ncclAllGather", &api.AllGather, &missing);
         all &= bind(lib, "ncclBroadcast", &api.Broadcast, &missing);
+        all &= bind(lib, "ncclAllReduce", &api.AllReduce, &missing);
         all &= bind(lib, "ncclGroupStart", &api.GroupStart, &missing);
         all &= bind(lib, "ncclGroupEnd", &api.GroupEnd, &missing);
         all &= bind(lib, "ncclGetErrorString", &api.GetErrorString, &missing);

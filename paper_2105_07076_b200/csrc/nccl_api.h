@@ -19,7 +19,10 @@ struct ncclUniqueId {
     char internal[128];
 };
 typedef int ncclResult_t;  // ncclSuccess = 0, ncclInProgress = 7
+constexpr int kNcclUint8 = 1;
+constexpr int kNcclInt32 = 2;
 constexpr int kNcclFloat64 = 8;
+constexpr int kNcclMin = 3;
 
 struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
@@ -29,6 +32,7 @@ struct NcclApi {
     ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;

@@ -266,6 +266,43 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ P, int64_t split
     }
 }
 
+// Sharded sketch with the all-gather fused in (idk_id_sharded's peer mode): the
+// split-K reduction writes each finished element of this rank's Y block to
+// every rank's Y buffer (f.y[g]: this rank's slot in rank g's buffer, mapped
+// over NVLink by CUDA IPC; f.y[0] is the local one), so the exchange rides on
+// the reduction's stores instead of a separate collective.  The system-scope
+// fence orders the remote stores before the kernel's completion, which the
+// caller's stream-ordered barrier then publishes.
+__global__ void splitk_reduce_fanout_kernel(const double* __restrict__ P, int64_t split_stride, int splits,
+                                            const FanOut f, int M, int64_t N, int64_t ldc) {
+    const int64_t total = static_cast<int64_t>(M) * N;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / M;
+        const int i = static_cast<int>(e - j * M);
+        const int64_t off = j * ldc + i;
+        double s = P[off];
+        for (int t = 1; t < splits; ++t) s += P[t * split_stride + off];
+#pragma unroll 1
+        for (int g = 0; g < f.count; ++g) f.y[g][off] = s;
+    }
+    __threadfence_system();
+}
+
+// splits == 1: the GEMM wrote f.y[0]; copy the block to the other destinations.
+__global__ void fanout_copy_kernel(const FanOut f, int M, int64_t N, int64_t ldc) {
+    const int64_t total = static_cast<int64_t>(M) * N;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = e / M;
+        const int64_t off = j * ldc + (e - j * M);
+        const double v = f.y[0][off];
+#pragma unroll 1
+        for (int g = 1; g < f.count; ++g) f.y[g][off] = v;
+    }
+    __threadfence_system();
+}
+
 // Grouped form: member g reduces the partials at P + g*group_stride into Ys[g].
 __global__ void splitk_reduce_group_kernel(const double* __restrict__ P, int64_t split_stride, int splits,
                                            int64_t group_stride, const GemmGroup grp, int M, int64_t N,
@@ -413,6 +450,39 @@ cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t l
     const int64_t total = static_cast<int64_t>(M) * N;
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
     splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(partial, split_stride, splits, Y, M, N, ldc);
+    return cudaGetLastError();
+}
+
+// Y block (M x N, ldc) = A * op(B) written to every f.y[g] (see
+// splitk_reduce_fanout_kernel); same arithmetic as sketch_gemm with `splits`.
+cudaError_t sketch_gemm_fanout(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans, const FanOut& f,
+                               int64_t ldc, int M, int64_t N, int64_t K, int splits, double* partial,
+                               cudaStream_t stream) {
+    if (M <= 0 || N <= 0 || f.count <= 0) return cudaSuccess;
+    if (f.count > kFanMax) return cudaErrorInvalidValue;
+    const int64_t total = static_cast<int64_t>(M) * N;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    if (splits <= 1) {
+        cudaError_t e = sketch_gemm(A, lda, B, ldb, b_trans, f.y[0], ldc, M, N, K, 1, nullptr, stream);
+        if (e != cudaSuccess || f.count == 1) return e;
+        fanout_copy_kernel<<<blocks, 256, 0, stream>>>(f, M, N, ldc);
+        return cudaGetLastError();
+    }
+    const int wm = sketch_gemm_pick_wm(M);
+    const bool vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+    const int64_t split_stride = ldc * N;
+    cudaError_t e = cudaErrorNotSupported;
+    const char* te = getenv("IDK_GEMM_TMA");
+    if (!te || atoi(te) != 0)
+        e = sketch_gemm_tma(A, lda, B, ldb, b_trans, partial, ldc, split_stride, M, N, K, splits, wm, stream);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        e = b_trans ? launch_nt<true>(wm, A, lda, B, ldb, partial, ldc, split_stride, M, N, K, splits, vec16, stream)
+                    : launch_nt<false>(wm, A, lda, B, ldb, partial, ldc, split_stride, M, N, K, splits, vec16, stream);
+    }
+    if (e != cudaSuccess) return e;
+    splitk_reduce_fanout_kernel<<<blocks, 256, 0, stream>>>(partial, split_stride, splits, f, M, N, ldc);
     return cudaGetLastError();
 }
 

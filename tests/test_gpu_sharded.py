@@ -94,3 +94,34 @@ def test_c_abi_id_sharded_one_rank_nccl_comm(oracle):
         ctx.comm_destroy()
     ref = idk.sketch_rid(a, 25, 5, seed=4)
     assert torch.equal(cols, ref.cols) and torch.equal(z, ref.z) and torch.equal(c, ref.c)
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+def test_sketch_fanout_writes_every_destination_bit_identical(oracle, transposed):
+    """The fused sketch + all-gather of the peer mode (idk_sketch_fanout): one
+    rank's block lands in every destination buffer (here three local buffers
+    standing in for three ranks' NVLink-mapped Y), bit-identical to the same
+    columns of the unsharded sketch (the split-K count of the full n)."""
+    import ctypes as C
+    import paper_2105_07076_b200 as idk
+    if transposed:
+        a = dev(oracle.gaussian_matrix(9000, 150, 12))  # M = A^T: 150 x 9000
+        m, n = 150, 9000
+    else:
+        a = dev(oracle.gaussian_matrix(2400, 7000, 12))
+        m, n = 2400, 7000
+    l, world = 40, 3
+    om = idk.sketch_omega(l, m, 5)
+    y_full = idk.sketch(om, a, transposed=transposed)
+    w = -(-n // world)
+    ctx = idk.context(0)
+    ctx.bind_stream()
+    bufs = [torch.full((world * w, l), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
+    for r in range(world):
+        b, e = column_range(n, world, r)
+        local = (a[b:e, :] if transposed else a[:, b:e]).t().contiguous().t()
+        dst = (C.c_void_p * world)(*[C.c_void_p(bf.data_ptr() + 8 * l * b) for bf in bufs])
+        ctx.check(ctx.lib.idk_sketch_fanout(ctx.h, C.c_void_p(om.data_ptr()), l, C.c_void_p(local.data_ptr()), m, e - b,
+                                            local.stride(1), 1 if transposed else 0, dst, world, l, n))
+    for bf in bufs:
+        assert torch.equal(bf[:n].t(), y_full)
