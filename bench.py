@@ -35,7 +35,7 @@ METRIC = "IDs/sec & achieved HBM GB/s / FP64 TFLOPS at 1/2/4/8 B200 vs CPU ref"
 UNIT = "IDs/s"
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
 
 
 def parse():

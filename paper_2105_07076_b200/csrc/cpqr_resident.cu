@@ -110,11 +110,13 @@ constexpr int max_threads_for() {
     return R >= 32 ? 512 : (R >= 16 ? 640 : 768);
 }
 
+#ifdef IDK_CPQR_TRACE
 __device__ __forceinline__ long long globaltimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+#endif
 
 // sqrt(v) >= (1 - 1e-14) * sqrt(vmax) (qr.cpp:71-73) evaluated exactly, with
 // the sqrt only inside the 4e-14 band where the answer is not obvious.
@@ -876,9 +878,13 @@ cpqr_resident_kernel(ResidentArgs a) {
     // Wait for every CTA's record of exchange `tag`, reduce them (identical in
     // every CTA), then copy the winner's column -- scaled by its reflector --
     // into xbuf.  `first` = the step the new pivot is for.
+#ifdef IDK_CPQR_TRACE
     unsigned epoch = 0;
+#endif
     auto grid_exchange = [&](int parity, unsigned tag, int first, bool cand, double lv, long long pos, int step) {
-        if (a.barrier != nullptr) grid_barrier(a.barrier, epoch);
+#ifdef IDK_CPQR_TRACE
+        if (a.barrier != nullptr) grid_barrier(a.barrier, epoch);  // debug builds: IDK_DEBUG_GRID_BARRIER
+#endif
         int slot = parity;
         // every thread polls at most a few records, all in flight at once:
         // one L2 round trip after the last arrival instead of one per record
