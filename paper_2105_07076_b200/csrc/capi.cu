@@ -198,7 +198,7 @@ CpqrWs carve_cpqr(Carve& cv, int64_t mrows, int64_t n, int64_t k, int num_sms, c
     if (ch.resident) pub = std::max(pub, idk::cpqr_resident_exchange_bytes(ch.plan, static_cast<int>(mrows)));
     w.pub = cv.take(pub);
     w.barrier = cv.take(sizeof(unsigned));
-    w.r11 = cv.take(sizeof(double) * k * k);
+    w.r11 = cv.take(idk::id_solve_z_scratch(static_cast<int>(k)));
     w.status = cv.take(sizeof(int));
     return w;
 }

@@ -76,6 +76,7 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
 
 // trsm.cu
 int id_trsm_nb(int k);
+size_t id_solve_z_scratch(int k);  // bytes of the R11 buffer id_solve_z needs
 size_t id_trsm_smem_bytes(int k);
 cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int64_t n, const long long* pivots,
                        const long long* pos, double* R11, int* status, double* Z, cudaStream_t stream);

@@ -209,45 +209,45 @@ id_trsm_dmma_kernel(const double* __restrict__ W, int64_t ldw, const double* __r
 // tile issued before the first DMMA) and each 32x32 diagonal block is staged
 // in shared memory for its substitution.  X (64 right-hand sides) and the
 // reciprocal diagonal live in shared memory.
-template <int NBLK>
-__global__ void __launch_bounds__(kDmmaThreads)
+template <int NBLK, int NB, int THR>
+__global__ void __launch_bounds__(THR)
 id_trsm_dmma_big_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ R11, int k, int64_t n,
                         const long long* __restrict__ pos, double* __restrict__ Z) {
     constexpr int KP = 32 * NBLK;
     constexpr int LD = KP + 4;
     constexpr int LDB = 32 + 1;  // diagonal block, column-major
     extern __shared__ __align__(16) double smem[];
-    double* Xs = smem;                     // kDmmaNB right-hand sides, stride LD
-    double* Db = Xs + kDmmaNB * LD;        // 32 x 32 diagonal block
+    double* Xs = smem;                     // NB right-hand sides, stride LD
+    double* Db = Xs + NB * LD;        // 32 x 32 diagonal block
     double* rinv = Db + 32 * LDB;          // KP
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int fr = lane >> 2, fc = lane & 3;
-    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kDmmaNB;
-    const int nb = static_cast<int>(min(static_cast<long long>(kDmmaNB), static_cast<long long>(n - c0)));
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * NB;
+    const int nb = static_cast<int>(min(static_cast<long long>(NB), static_cast<long long>(n - c0)));
     // R[row, col] with the identity padding beyond k
     auto rget = [&](int row, int col) -> double {
         return (row < k && col < k) ? __ldg(R11 + static_cast<int64_t>(col) * k + row) : (row == col ? 1.0 : 0.0);
     };
 
-    for (int e = tid; e < kDmmaNB * KP; e += kDmmaThreads) {
+    for (int e = tid; e < NB * KP; e += THR) {
         const int c = e / KP, row = e - c * KP;
         double* dst = Xs + c * LD + row;
         if (c < nb && row < k) cp_async_8(dst, W + (c0 + c) * ldw + row);
         else *dst = 0.0;
     }
-    for (int row = tid; row < KP; row += kDmmaThreads) rinv[row] = 1.0 / rget(row, row);
+    for (int row = tid; row < KP; row += THR) rinv[row] = 1.0 / rget(row, row);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
 
 #pragma unroll 1
     for (int b = NBLK - 1; b >= 0; --b) {
         const int r0 = 32 * b;
-        for (int e = tid; e < 32 * 32; e += kDmmaThreads) {
+        for (int e = tid; e < 32 * 32; e += THR) {
             const int col = e >> 5, row = e & 31;
             Db[col * LDB + row] = rget(r0 + row, r0 + col);
         }
         __syncthreads();
-        if (tid < kDmmaNB) {
+        if (tid < NB) {
             double x[32];
             double* xc = Xs + tid * LD + r0;
 #pragma unroll
@@ -262,14 +262,14 @@ id_trsm_dmma_big_kernel(const double* __restrict__ W, int64_t ldw, const double*
             for (int r = 0; r < 32; ++r) xc[r] = x[r];
         }
         __syncthreads();
-        for (int rt = warp; rt < 4 * b; rt += kDmmaThreads / 32) {
+        for (int rt = warp; rt < 4 * b; rt += THR / 32) {
             const int row = rt * 8 + fr;
             double af[8];
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) af[ks] = -rget(row, r0 + ks * 4 + fc);
-            double acc[kDmmaNB / 8][2];
+            double acc[NB / 8][2];
 #pragma unroll
-            for (int ct = 0; ct < kDmmaNB / 8; ++ct) {
+            for (int ct = 0; ct < NB / 8; ++ct) {
                 acc[ct][0] = Xs[(ct * 8 + 2 * fc) * LD + row];
                 acc[ct][1] = Xs[(ct * 8 + 2 * fc + 1) * LD + row];
             }
@@ -277,10 +277,10 @@ id_trsm_dmma_big_kernel(const double* __restrict__ W, int64_t ldw, const double*
             for (int ks = 0; ks < 8; ++ks) {
                 const int kk = r0 + ks * 4 + fc;
 #pragma unroll
-                for (int ct = 0; ct < kDmmaNB / 8; ++ct) dmma_8x8x4(acc[ct], af[ks], Xs[(ct * 8 + fr) * LD + kk]);
+                for (int ct = 0; ct < NB / 8; ++ct) dmma_8x8x4(acc[ct], af[ks], Xs[(ct * 8 + fr) * LD + kk]);
             }
 #pragma unroll
-            for (int ct = 0; ct < kDmmaNB / 8; ++ct) {
+            for (int ct = 0; ct < NB / 8; ++ct) {
                 Xs[(ct * 8 + 2 * fc) * LD + row] = acc[ct][0];
                 Xs[(ct * 8 + 2 * fc + 1) * LD + row] = acc[ct][1];
             }
@@ -288,12 +288,12 @@ id_trsm_dmma_big_kernel(const double* __restrict__ W, int64_t ldw, const double*
         __syncthreads();
     }
 
-    constexpr int kPer = kDmmaNB / (kDmmaThreads / 32);
-    const long long mp = (lane < kPer && warp + (kDmmaThreads / 32) * lane < nb)
-                             ? pos[c0 + warp + (kDmmaThreads / 32) * lane] : 0;
+    constexpr int kPer = NB / (THR / 32);
+    const long long mp = (lane < kPer && warp + (THR / 32) * lane < nb)
+                             ? pos[c0 + warp + (THR / 32) * lane] : 0;
 #pragma unroll 4
     for (int t = 0; t < kPer; ++t) {
-        const int c = warp + (kDmmaThreads / 32) * t;
+        const int c = warp + (THR / 32) * t;
         const long long p = __shfl_sync(0xffffffffu, mp, t);
         if (c < nb) {
             const int64_t col = c0 + c;
@@ -302,17 +302,180 @@ id_trsm_dmma_big_kernel(const double* __restrict__ W, int64_t ldw, const double*
     }
 }
 
+template <int NBLK, int NB, int THR>
+cudaError_t launch_trsm_dmma_big_nb(const double* W, int64_t ldw, const double* R11, int k, int64_t n,
+                                    const long long* pos, double* Z, cudaStream_t stream) {
+    constexpr int KP = 32 * NBLK, LD = KP + 4;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(NB) * LD + 32 * 33 + KP);
+    cudaError_t e = cudaFuncSetAttribute(id_trsm_dmma_big_kernel<NBLK, NB, THR>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (n + NB - 1) / NB;
+    id_trsm_dmma_big_kernel<NBLK, NB, THR><<<static_cast<unsigned>(blocks), THR, smem, stream>>>(W, ldw, R11, k, n,
+                                                                                                 pos, Z);
+    return cudaGetLastError();
+}
+
+// Right-hand sides per CTA and threads: NB = 56 makes the 16384-column cfg4
+// solve two nearly full waves of one CTA per SM (293 CTAs; 64 leaves the second
+// wave 73 % full), and 8 warps share the DMMA row tiles of each block column
+// (profiles/trsm_r02.txt).  IDK_TRSM_BIG=<nb> selects 64 / 56 / 48 / 32 for A/B.
 template <int NBLK>
 cudaError_t launch_trsm_dmma_big(const double* W, int64_t ldw, const double* R11, int k, int64_t n,
                                  const long long* pos, double* Z, cudaStream_t stream) {
+    const char* ev = getenv("IDK_TRSM_BIG");
+    const int sel = ev ? atoi(ev) : 56;
+    switch (sel) {
+        case 64: return launch_trsm_dmma_big_nb<NBLK, 64, 128>(W, ldw, R11, k, n, pos, Z, stream);
+        case 65: return launch_trsm_dmma_big_nb<NBLK, 64, 256>(W, ldw, R11, k, n, pos, Z, stream);
+        case 48: return launch_trsm_dmma_big_nb<NBLK, 48, 192>(W, ldw, R11, k, n, pos, Z, stream);
+        case 32: return launch_trsm_dmma_big_nb<NBLK, 32, 128>(W, ldw, R11, k, n, pos, Z, stream);
+        default: return launch_trsm_dmma_big_nb<NBLK, 56, 256>(W, ldw, R11, k, n, pos, Z, stream);
+    }
+}
+
+// Inverses of the 32 x 32 diagonal blocks of R11 (identity beyond k), one CTA
+// of 32 threads per block: thread j solves D x = e_j by back substitution
+// (solve.cpp:43-51's order and divisions).  Dinv[b] is column-major, ld 32.
+__global__ void __launch_bounds__(32) invert_diag_blocks_kernel(const double* __restrict__ R11, int k,
+                                                                 double* __restrict__ Dinv) {
+    const int b = blockIdx.x, j = threadIdx.x, r0 = 32 * b;
+    __shared__ double D[32][33];
+    for (int c = 0; c < 32; ++c) {
+        const int row = r0 + j, col = r0 + c;
+        D[j][c] = (row < k && col < k) ? R11[static_cast<int64_t>(col) * k + row] : (row == col ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    double x[32];
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+        double acc = i == j ? 1.0 : 0.0;
+#pragma unroll
+        for (int l = i + 1; l < 32; ++l) acc -= D[i][l] * x[l];
+        x[i] = acc / D[i][i];
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) Dinv[static_cast<int64_t>(b) * 1024 + j * 32 + i] = x[i];
+}
+
+// k in (128, 256] without the serial substitution: per 32-row block
+// (bottom-up) X_b <- Dinv_b X_b and X_above -= R_above,b X_b, both on the DMMA
+// pipe, so every warp works in every phase (the substitution kept one or two
+// warps busy while the others waited at the barrier).
+template <int NBLK, int NB, int THR>
+__global__ void __launch_bounds__(THR)
+id_trsm_dinv_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ R11,
+                    const double* __restrict__ Dinv, int k, int64_t n, const long long* __restrict__ pos,
+                    double* __restrict__ Z) {
+    constexpr int KP = 32 * NBLK;
+    constexpr int LD = KP + 4;
+    constexpr int LDB = 32 + 4;  // Dinv block, column-major: fragment loads bank-conflict free
+    constexpr int NW = THR / 32;
+    constexpr int CT = NB / 8;    // 8-column tiles
+    extern __shared__ __align__(16) double smem[];
+    double* Xs = smem;            // NB right-hand sides, stride LD
+    double* Db = Xs + NB * LD;    // 32 x 32 inverse diagonal block
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.x) * NB;
+    const int nb = static_cast<int>(min(static_cast<long long>(NB), static_cast<long long>(n - c0)));
+    auto rget = [&](int row, int col) -> double {
+        return (row < k && col < k) ? __ldg(R11 + static_cast<int64_t>(col) * k + row) : (row == col ? 1.0 : 0.0);
+    };
+    for (int e = tid; e < NB * KP; e += THR) {
+        const int c = e / KP, row = e - c * KP;
+        double* dst = Xs + c * LD + row;
+        if (c < nb && row < k) cp_async_8(dst, W + (c0 + c) * ldw + row);
+        else *dst = 0.0;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+
+#pragma unroll 1
+    for (int b = NBLK - 1; b >= 0; --b) {
+        const int r0 = 32 * b;
+        for (int e = tid; e < 32 * 32; e += THR) Db[(e >> 5) * LDB + (e & 31)] = __ldg(Dinv + b * 1024 + e);
+        __syncthreads();
+        // X_b <- Dinv_b X_b: 4 row tiles x CT column tiles, k-depth 32
+        constexpr int kTiles = 4 * CT;
+        double acc[(kTiles + NW - 1) / NW][2];
+#pragma unroll
+        for (int t = 0; t < (kTiles + NW - 1) / NW; ++t) {
+            acc[t][0] = acc[t][1] = 0.0;
+            const int tile = warp + NW * t;
+            if (tile < kTiles) {
+                const int rt = tile / CT, ct = tile - rt * CT;
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const int kk = ks * 4 + fc;
+                    dmma_8x8x4(acc[t], Db[kk * LDB + rt * 8 + fr], Xs[(ct * 8 + fr) * LD + r0 + kk]);
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < (kTiles + NW - 1) / NW; ++t) {
+            const int tile = warp + NW * t;
+            if (tile < kTiles) {
+                const int rt = tile / CT, ct = tile - rt * CT;
+                const int row = r0 + rt * 8 + fr;
+                Xs[(ct * 8 + 2 * fc) * LD + row] = acc[t][0];
+                Xs[(ct * 8 + 2 * fc + 1) * LD + row] = acc[t][1];
+            }
+        }
+        __syncthreads();
+        // rows [0, r0) -= R[0:r0, block b] X_b
+        for (int rt = warp; rt < 4 * b; rt += NW) {
+            const int row = rt * 8 + fr;
+            double af[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) af[ks] = -rget(row, r0 + ks * 4 + fc);
+            double ac[CT][2];
+#pragma unroll
+            for (int ct = 0; ct < CT; ++ct) {
+                ac[ct][0] = Xs[(ct * 8 + 2 * fc) * LD + row];
+                ac[ct][1] = Xs[(ct * 8 + 2 * fc + 1) * LD + row];
+            }
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int kk = r0 + ks * 4 + fc;
+#pragma unroll
+                for (int ct = 0; ct < CT; ++ct) dmma_8x8x4(ac[ct], af[ks], Xs[(ct * 8 + fr) * LD + kk]);
+            }
+#pragma unroll
+            for (int ct = 0; ct < CT; ++ct) {
+                Xs[(ct * 8 + 2 * fc) * LD + row] = ac[ct][0];
+                Xs[(ct * 8 + 2 * fc + 1) * LD + row] = ac[ct][1];
+            }
+        }
+        __syncthreads();
+    }
+
+    constexpr int kPer = NB / NW;
+    const long long mp = (lane < kPer && warp + NW * lane < nb) ? pos[c0 + warp + NW * lane] : 0;
+#pragma unroll 4
+    for (int t = 0; t < kPer; ++t) {
+        const int c = warp + NW * t;
+        const long long p = __shfl_sync(0xffffffffu, mp, t);
+        if (c < nb) {
+            const int64_t col = c0 + c;
+            for (int i = lane; i < k; i += 32) Z[col * k + i] = p < k ? (i == p ? 1.0 : 0.0) : Xs[c * LD + i];
+        }
+    }
+}
+
+template <int NBLK, int NB, int THR>
+cudaError_t launch_trsm_dinv(const double* W, int64_t ldw, const double* R11, double* Dinv, int k, int64_t n,
+                             const long long* pos, double* Z, cudaStream_t stream) {
+    invert_diag_blocks_kernel<<<NBLK, 32, 0, stream>>>(R11, k, Dinv);
     constexpr int KP = 32 * NBLK, LD = KP + 4;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(kDmmaNB) * LD + 32 * 33 + KP);
-    cudaError_t e = cudaFuncSetAttribute(id_trsm_dmma_big_kernel<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem = sizeof(double) * (static_cast<size_t>(NB) * LD + 32 * 36);
+    cudaError_t e = cudaFuncSetAttribute(id_trsm_dinv_kernel<NBLK, NB, THR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    const int64_t blocks = (n + kDmmaNB - 1) / kDmmaNB;
-    id_trsm_dmma_big_kernel<NBLK><<<static_cast<unsigned>(blocks), kDmmaThreads, smem, stream>>>(W, ldw, R11, k, n,
-                                                                                                   pos, Z);
+    const int64_t blocks = (n + NB - 1) / NB;
+    id_trsm_dinv_kernel<NBLK, NB, THR><<<static_cast<unsigned>(blocks), THR, smem, stream>>>(W, ldw, R11, Dinv, k, n,
+                                                                                             pos, Z);
     return cudaGetLastError();
 }
 
@@ -573,6 +736,11 @@ __global__ void copy_pivots_kernel(const long long* __restrict__ src, int k, lon
 
 }  // namespace
 
+// R11 buffer of id_solve_z: k x k, then the inverse diagonal blocks (k > 128).
+size_t id_solve_z_scratch(int k) {
+    return sizeof(double) * (static_cast<size_t>(k) * k + 1024 * static_cast<size_t>((k + 31) / 32));
+}
+
 // Right-hand sides per CTA: 32 while the k x 32 tile fits in ~160 KB.
 int id_trsm_nb(int k) {
     const int cap = static_cast<int>((160 * 1024 / sizeof(double)) / (k | 1));
@@ -598,6 +766,22 @@ cudaError_t id_solve_z(const double* W, int64_t ldw, int k, int64_t c_begin, int
             case 2: return launch_trsm_dmma<2>(W, ldw, R11, k, n, pos, Z, stream);
             case 3: return launch_trsm_dmma<3>(W, ldw, R11, k, n, pos, Z, stream);
             default: return launch_trsm_dmma<4>(W, ldw, R11, k, n, pos, Z, stream);
+        }
+    }
+    const char* tv = getenv("IDK_TRSM_DINV");
+    if (k > 128 && k <= 256 && !(te && atoi(te) == 0) && !(tv && atoi(tv) == 0)) {
+        double* Dinv = R11 + static_cast<int64_t>(k) * k;  // carved after R11 (id_solve_z_scratch)
+        const char* nbv = getenv("IDK_TRSM_NB");
+        const int nbsel = nbv ? atoi(nbv) : 64;  // profiles/trsm_r02.txt
+        switch ((k + 31) / 32) {
+#define IDK_DINV(NBLK)                                                                                           \
+    case NBLK:                                                                                                   \
+        if (nbsel == 64) return launch_trsm_dinv<NBLK, 64, 256>(W, ldw, R11, Dinv, k, n, pos, Z, stream);         \
+        if (nbsel == 16) return launch_trsm_dinv<NBLK, 16, 128>(W, ldw, R11, Dinv, k, n, pos, Z, stream);         \
+        return launch_trsm_dinv<NBLK, 32, 128>(W, ldw, R11, Dinv, k, n, pos, Z, stream);
+            IDK_DINV(5) IDK_DINV(6) IDK_DINV(7) IDK_DINV(8)
+#undef IDK_DINV
+            default: break;
         }
     }
     if (k <= 256 && !(te && atoi(te) == 0)) {
