@@ -697,6 +697,23 @@ __global__ void gather_columns_vec_kernel(const double* __restrict__ A, int64_t 
 // A CTA takes 32 values of i: warp w reads A[cols[j], i0 + lane] for its j's
 // (32 consecutive i of one row: 32 strided sectors), stages a 32 x k tile in
 // shared memory, and writes C coalesced along i.
+template <int LV>
+__device__ __forceinline__ double ld_row_elem(const double* p) {
+    if constexpr (LV == 1) return __ldg(p);
+    if constexpr (LV == 2) {
+        double v;
+        asm volatile("ld.global.L1::no_allocate.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+        return v;
+    }
+    if constexpr (LV == 3) {
+        double v;
+        asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+        return v;
+    }
+    return __ldcs(p);
+}
+
+template <int LV>
 __global__ void gather_rows_kernel(const double* __restrict__ A, int64_t lda, int64_t n,
                                    const long long* __restrict__ cols, int k, double* __restrict__ C) {
     extern __shared__ double tile[];  // k x 33
@@ -707,11 +724,11 @@ __global__ void gather_rows_kernel(const double* __restrict__ A, int64_t lda, in
     for (; j + 3 * nw < k; j += 4 * nw) {  // four independent sector reads in flight per thread
         double v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = i < n ? __ldcs(A + cols[j + u * nw] + i * lda) : 0.0;
+        for (int u = 0; u < 4; ++u) v[u] = i < n ? ld_row_elem<LV>(A + cols[j + u * nw] + i * lda) : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) tile[(j + u * nw) * 33 + lane] = v[u];
     }
-    for (; j < k; j += nw) tile[j * 33 + lane] = i < n ? __ldcs(A + cols[j] + i * lda) : 0.0;
+    for (; j < k; j += nw) tile[j * 33 + lane] = i < n ? ld_row_elem<LV>(A + cols[j] + i * lda) : 0.0;
     __syncthreads();
     for (int j = wid; j < k; j += nw)
         if (i < n) __stcs(C + static_cast<int64_t>(j) * n + i, tile[j * 33 + lane]);
@@ -850,13 +867,20 @@ cudaError_t gather_columns(const double* A, int64_t lda, int64_t rows, const lon
     }
     if (rows_of_a && sizeof(double) * static_cast<size_t>(k) * 33 <= 200 * 1024) {
         const size_t smem = sizeof(double) * static_cast<size_t>(k) * 33;
+        // loads with the .L2::64B prefetch size: each scattered 8-byte element
+        // costs a 64-byte L2 fill instead of 128 (cfg5: 33.6 -> 16.8 MB of DRAM reads
+        // for 2.1 MB of C; profiles/gather_rows_r02.txt).  IDK_GATHER_ROWS_LD selects
+        // the other load forms for A/B.
+        const char* lv = getenv("IDK_GATHER_ROWS_LD");
+        const int sel = lv ? atoi(lv) : 2;
+        auto kern = sel == 1 ? gather_rows_kernel<1> : sel == 2 ? gather_rows_kernel<2>
+                  : sel == 3 ? gather_rows_kernel<3> : gather_rows_kernel<0>;
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  static_cast<int>(smem));
             if (e != cudaSuccess) return e;
         }
-        gather_rows_kernel<<<static_cast<unsigned>((rows + 31) / 32), k >= 256 ? 256 : 128, smem, stream>>>(
-            A, lda, rows, cols, k, C);
+        kern<<<static_cast<unsigned>((rows + 31) / 32), k >= 256 ? 256 : 128, smem, stream>>>(A, lda, rows, cols, k, C);
         return cudaGetLastError();
     }
     gather_columns_kernel<<<static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8)), 256, 0, stream>>>(
