@@ -208,6 +208,25 @@ IDK_API int idk_comm_init(idk_handle h, int nranks, int rank, const void* id128)
 IDK_API int idk_set_nccl_comm(idk_handle h, void* nccl_comm);
 IDK_API int idk_comm_destroy(idk_handle h);
 
+/* A caller-supplied transport instead of NCCL (MPI, a test harness, ...):
+ * host-memory collectives over the ranks, each returning 0 on success.
+ * allgather: every rank's `bytes` from send, concatenated in rank order into
+ * recv; broadcast: root's `bytes` of buf to every rank; barrier.  The library
+ * synchronises its stream and stages device buffers through host memory
+ * around each call.  NULL removes them.  An NCCL communicator, when set,
+ * takes precedence. */
+typedef struct {
+    void* ctx;
+    int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes);
+    int (*broadcast)(void* ctx, void* buf, uint64_t bytes, int root);
+    int (*barrier)(void* ctx);
+} idk_host_collectives;
+IDK_API int idk_set_host_collectives(idk_handle h, int nranks, int rank, const idk_host_collectives* c);
+/* How idk_id_sharded exchanged Y on this handle: 1 = peer mode (fused into the
+ * sketch over CUDA IPC mappings), -1 = all-gather (IPC unavailable or
+ * IDK_SHARD_P2P=0), 0 = not yet decided (no multi-rank call so far). */
+IDK_API int idk_shard_peer_mode(idk_handle h);
+
 /* Sharded Gaussian-sketch RID (the north-star path over nranks GPUs; cfg4 /
  * cfg5).  Every rank passes its block of M's columns [begin, end) from
  * idk_shard_range: d_a_local is m x (end-begin) (lda >= m), or with

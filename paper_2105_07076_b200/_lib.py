@@ -59,6 +59,8 @@ SIGNATURES = {
     "idk_comm_init": (C.c_int, [_P, C.c_int, C.c_int, _P]),
     "idk_set_nccl_comm": (C.c_int, [_P, _P]),
     "idk_comm_destroy": (C.c_int, [_P]),
+    "idk_set_host_collectives": (C.c_int, [_P, C.c_int, C.c_int, _P]),
+    "idk_shard_peer_mode": (C.c_int, [_P]),
     "idk_sketch_fanout": (C.c_int, [_P, _P, _I64, _P, _I64, _I64, _I64, C.c_int, _P, C.c_int, _I64, _I64]),
     "idk_id_sharded": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, _I64, _I64, C.c_uint64, C.c_int, _P, _P, _P, _P]),
     "idk_id_auto_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.c_int, C.c_uint64, _I64, C.c_int, _P, _P, _P,

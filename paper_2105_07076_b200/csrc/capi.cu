@@ -73,6 +73,9 @@ struct idk_context {
     double* peer_y[idk::kFanMax] = {};
     int* d_flag = nullptr;   // 1-int scratch of the stream-ordered barrier / agreement
     int p2p_state = 0;       // 0 untried, 1 on, -1 off (IPC unavailable: the NCCL all-gather runs)
+    // caller-supplied host collectives (idk_set_host_collectives), used when no NCCL communicator is set
+    idk_host_collectives hc = {};
+    bool has_hc = false;
 };
 
 namespace {
@@ -1550,6 +1553,20 @@ int idk_id_auto_host(idk_handle h, const double* h_a, int64_t m, int64_t n, int6
 
 // ---- multi-GPU: column-sharded ID over NCCL ----------
 
+// A new communicator / transport invalidates the peer mappings of the old one.
+static void reset_peers(idk_handle h) {
+    cudaStreamSynchronize(h->stream);
+    for (int g = 0; g < idk::kFanMax; ++g) {
+        if (h->peer_y[g] && h->peer_y[g] != h->ybuf) cudaIpcCloseMemHandle(h->peer_y[g]);
+        h->peer_y[g] = nullptr;
+    }
+    if (h->ybuf) cudaFree(h->ybuf);
+    h->ybuf = nullptr;
+    h->ybuf_cap = 0;
+    h->p2p_state = 0;
+    h->has_hc = false;
+}
+
 int idk_shard_range(int64_t n, int nranks, int rank, int64_t* begin, int64_t* end) {
     if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || !begin || !end) return IDK_ERR_INVALID_ARG;
     const int64_t w = (n + nranks - 1) / nranks;
@@ -1575,6 +1592,7 @@ int idk_comm_init(idk_handle h, int nranks, int rank, const void* id128) {
     const idk::NcclApi* api = idk::nccl_api(&e);
     if (!api) return set_err(h, IDK_ERR_NCCL, "comm_init: " + e);
     cudaSetDevice(h->device);
+    reset_peers(h);
     if (h->nccl_comm && h->nccl_owned) api->CommDestroy(h->nccl_comm);
     h->nccl_comm = nullptr;
     idk::ncclUniqueId id;
@@ -1594,6 +1612,7 @@ int idk_set_nccl_comm(idk_handle h, void* nccl_comm) {
     std::string e;
     const idk::NcclApi* api = idk::nccl_api(&e);
     if (!api) return set_err(h, IDK_ERR_NCCL, "set_nccl_comm: " + e);
+    reset_peers(h);
     if (h->nccl_comm && h->nccl_owned) api->CommDestroy(h->nccl_comm);
     h->nccl_comm = static_cast<idk::ncclComm_t>(nccl_comm);
     h->nccl_owned = false;
@@ -1611,6 +1630,7 @@ int idk_set_nccl_comm(idk_handle h, void* nccl_comm) {
 
 int idk_comm_destroy(idk_handle h) {
     if (!h) return IDK_ERR_INVALID_ARG;
+    reset_peers(h);
     if (h->nccl_comm && h->nccl_owned) {
         if (const idk::NcclApi* api = idk::nccl_api(nullptr)) api->CommDestroy(h->nccl_comm);
     }
@@ -1642,11 +1662,83 @@ int idk_sketch_fanout(idk_handle h, const double* d_omega, int64_t l, const doub
     return IDK_OK;
 }
 
-// Peer mode setup (collective over the communicator): (re)allocate this rank's
-// Y buffer, all-gather the CUDA IPC handles with NCCL, open the peers'
-// buffers, and agree (NCCL min) that every rank succeeded -- otherwise every
-// rank falls back to the NCCL all-gather together.
-static int peer_setup(idk_handle h, const idk::NcclApi* api, size_t bytes) {
+// The collectives of idk_id_sharded: NCCL on the handle's stream (stream-ordered),
+// or the caller's host collectives (idk_set_host_collectives: the stream is
+// synchronised and buffers staged through host memory around each call).
+struct Coll {
+    idk_context* h;
+    const idk::NcclApi* api;  // null: host collectives
+    int fail(const char* what, int r) {
+        return set_err(h, IDK_ERR_NCCL, std::string(what) + ": " + (api ? api->GetErrorString(r) : "host collective failed"));
+    }
+    // every rank's `bytes` at d_send, concatenated in rank order into d_recv (device)
+    int allgather(const void* d_send, void* d_recv, size_t bytes) {
+        if (api) {
+            const idk::ncclResult_t r = api->AllGather(d_send, d_recv, bytes, idk::kNcclUint8, h->nccl_comm, h->stream);
+            return r ? fail("ncclAllGather", r) : IDK_OK;
+        }
+        std::vector<char> snd(bytes), rcv(bytes * static_cast<size_t>(h->nranks));
+        IDK_CUDA(cudaMemcpyAsync(snd.data(), d_send, bytes, cudaMemcpyDeviceToHost, h->stream));
+        IDK_CUDA(cudaStreamSynchronize(h->stream));
+        if (h->hc.allgather(h->hc.ctx, snd.data(), rcv.data(), bytes)) return fail("allgather", 0);
+        IDK_CUDA(cudaMemcpyAsync(d_recv, rcv.data(), rcv.size(), cudaMemcpyHostToDevice, h->stream));
+        IDK_CUDA(cudaStreamSynchronize(h->stream));
+        return IDK_OK;
+    }
+    // every rank sees the minimum of `v` over the ranks (host ints)
+    int agree_min(int v, int* out) {
+        if (api) {
+            IDK_CUDA(cudaMemcpyAsync(h->d_flag, &v, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+            const idk::ncclResult_t r =
+                api->AllReduce(h->d_flag, h->d_flag, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
+            if (r) return fail("ncclAllReduce", r);
+            IDK_CUDA(cudaMemcpyAsync(out, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+            IDK_CUDA(cudaStreamSynchronize(h->stream));
+            return IDK_OK;
+        }
+        std::vector<int> all(static_cast<size_t>(h->nranks));
+        if (h->hc.allgather(h->hc.ctx, &v, all.data(), sizeof(int))) return fail("allgather", 0);
+        *out = *std::min_element(all.begin(), all.end());
+        return IDK_OK;
+    }
+    // every rank's work queued so far has finished before any rank's later work starts
+    int barrier() {
+        if (api) {
+            const idk::ncclResult_t r =
+                api->AllReduce(h->d_flag, h->d_flag + 1, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
+            return r ? fail("ncclAllReduce (barrier)", r) : IDK_OK;
+        }
+        IDK_CUDA(cudaStreamSynchronize(h->stream));
+        return h->hc.barrier(h->hc.ctx) ? fail("barrier", 0) : IDK_OK;
+    }
+    // C's columns from their owners (column j from rank owner[j]); d_c is m x k on every rank
+    int columns_from_owners(double* d_c, int64_t m, int64_t k, const std::vector<int>& owner) {
+        if (api) {
+            for (int64_t j0 = 0; j0 < k; j0 += 512) {
+                api->GroupStart();
+                for (int64_t j = j0; j < std::min<int64_t>(k, j0 + 512); ++j)
+                    api->Broadcast(d_c + j * m, d_c + j * m, static_cast<size_t>(m), idk::kNcclFloat64, owner[j],
+                                   h->nccl_comm, h->stream);
+                const idk::ncclResult_t r = api->GroupEnd();
+                if (r) return fail("ncclBroadcast", r);
+            }
+            return IDK_OK;
+        }
+        std::vector<double> hc(static_cast<size_t>(m * k));
+        IDK_CUDA(cudaMemcpyAsync(hc.data(), d_c, sizeof(double) * m * k, cudaMemcpyDeviceToHost, h->stream));
+        IDK_CUDA(cudaStreamSynchronize(h->stream));
+        for (int64_t j = 0; j < k; ++j)
+            if (h->hc.broadcast(h->hc.ctx, hc.data() + j * m, sizeof(double) * m, owner[j])) return fail("broadcast", 0);
+        IDK_CUDA(cudaMemcpyAsync(d_c, hc.data(), sizeof(double) * m * k, cudaMemcpyHostToDevice, h->stream));
+        return IDK_OK;
+    }
+};
+
+// Peer mode setup (collective): (re)allocate this rank's Y buffer, all-gather
+// the CUDA IPC handles, open the peers' buffers, and agree (min over ranks)
+// that every rank succeeded -- otherwise every rank falls back to the
+// all-gather of Y together.
+static int peer_setup(idk_handle h, Coll& co, size_t bytes) {
     const int G = h->nranks;
     if (h->p2p_state == -1) return IDK_OK;
     if (h->p2p_state == 1 && bytes <= h->ybuf_cap) return IDK_OK;
@@ -1663,7 +1755,6 @@ static int peer_setup(idk_handle h, const idk::NcclApi* api, size_t bytes) {
     if (h->ybuf) cudaFree(h->ybuf);
     h->ybuf = nullptr;
     h->ybuf_cap = 0;
-    if (!h->d_flag) IDK_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->d_flag), 2 * sizeof(int)));
     int ok = 1;
     cudaIpcMemHandle_t mine;
     std::memset(&mine, 0, sizeof(mine));
@@ -1677,11 +1768,10 @@ static int peer_setup(idk_handle h, const idk::NcclApi* api, size_t bytes) {
     IDK_CUDA(cudaMalloc(reinterpret_cast<void**>(&d_h), sizeof(cudaIpcMemHandle_t) * (G + 1)));
     IDK_CUDA(cudaMemcpyAsync(d_h + sizeof(cudaIpcMemHandle_t) * h->rank, &mine, sizeof(mine), cudaMemcpyHostToDevice,
                              h->stream));
-    idk::ncclResult_t r = api->AllGather(d_h + sizeof(cudaIpcMemHandle_t) * h->rank, d_h, sizeof(cudaIpcMemHandle_t),
-                                         idk::kNcclUint8, h->nccl_comm, h->stream);
-    if (r != 0) {
+    int rc = co.allgather(d_h + sizeof(cudaIpcMemHandle_t) * h->rank, d_h, sizeof(cudaIpcMemHandle_t));
+    if (rc) {
         cudaFree(d_h);
-        return set_err(h, IDK_ERR_NCCL, std::string("ncclAllGather (IPC handles): ") + api->GetErrorString(r));
+        return rc;
     }
     IDK_CUDA(cudaMemcpyAsync(all.data(), d_h, sizeof(cudaIpcMemHandle_t) * G, cudaMemcpyDeviceToHost, h->stream));
     IDK_CUDA(cudaStreamSynchronize(h->stream));
@@ -1699,13 +1789,8 @@ static int peer_setup(idk_handle h, const idk::NcclApi* api, size_t bytes) {
             h->peer_y[g] = static_cast<double*>(p);
         }
     }
-    // every rank must take the same path
-    IDK_CUDA(cudaMemcpyAsync(h->d_flag, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-    r = api->AllReduce(h->d_flag, h->d_flag, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
-    if (r != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllReduce: ") + api->GetErrorString(r));
     int all_ok = 0;
-    IDK_CUDA(cudaMemcpyAsync(&all_ok, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    IDK_CUDA(cudaStreamSynchronize(h->stream));
+    if ((rc = co.agree_min(ok, &all_ok))) return rc;  // every rank must take the same path
     if (!all_ok) {
         for (int g = 0; g < idk::kFanMax; ++g) {
             if (h->peer_y[g] && h->peer_y[g] != h->ybuf) cudaIpcCloseMemHandle(h->peer_y[g]);
@@ -1721,6 +1806,26 @@ static int peer_setup(idk_handle h, const idk::NcclApi* api, size_t bytes) {
     return IDK_OK;
 }
 
+int idk_shard_peer_mode(idk_handle h) { return h ? h->p2p_state : 0; }
+
+int idk_set_host_collectives(idk_handle h, int nranks, int rank, const idk_host_collectives* c) {
+    if (!h || nranks < 1 || rank < 0 || rank >= nranks) return IDK_ERR_INVALID_ARG;
+    if (c && (!c->allgather || !c->broadcast || !c->barrier))
+        return set_err(h, IDK_ERR_INVALID_ARG, "set_host_collectives: every callback is required");
+    reset_peers(h);
+    if (h->nccl_comm && h->nccl_owned) {
+        if (const idk::NcclApi* api = idk::nccl_api(nullptr)) api->CommDestroy(h->nccl_comm);
+    }
+    h->nccl_comm = nullptr;
+    h->nccl_owned = false;
+    h->has_hc = c != nullptr;
+    if (c) h->hc = *c;
+    h->nranks = c ? nranks : 1;
+    h->rank = c ? rank : 0;
+    h->p2p_state = 0;
+    return IDK_OK;
+}
+
 int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, int64_t lda, int a_transposed,
                    int64_t k, int64_t p, uint64_t seed, int omega_mode, const double* d_omega, int64_t* d_cols,
                    double* d_z_local, double* d_c) {
@@ -1733,11 +1838,14 @@ int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, 
         return set_err(h, IDK_ERR_INVALID_ARG, "id_sharded: bad omega mode");
     const int G = h->nranks, r = h->rank;
     const idk::NcclApi* api = nullptr;
-    if (G > 1) {
+    if (G > 1 && h->nccl_comm) {
         std::string e;
-        if (!h->nccl_comm || !(api = idk::nccl_api(&e)))
-            return set_err(h, IDK_ERR_NCCL, "id_sharded: no NCCL communicator (idk_comm_init) " + e);
+        if (!(api = idk::nccl_api(&e))) return set_err(h, IDK_ERR_NCCL, "id_sharded: " + e);
+    } else if (G > 1 && !h->has_hc) {
+        return set_err(h, IDK_ERR_NCCL, "id_sharded: no communicator (idk_comm_init / idk_set_host_collectives)");
     }
+    if (G > 1 && !h->d_flag) IDK_CUDA(cudaMalloc(reinterpret_cast<void**>(&h->d_flag), 2 * sizeof(int)));
+    Coll co{h, api};
     int64_t b = 0, e_ = 0;
     idk_shard_range(n, G, r, &b, &e_);
     const int64_t w = (n + G - 1) / G, nr = e_ - b;
@@ -1752,7 +1860,7 @@ int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, 
     // the same order as on one GPU, so the sharded result is bit-identical
     const int splits = idk::sketch_gemm_pick_splits(static_cast<int>(l), n, m, h->num_sms);
     const size_t ybytes = sizeof(double) * l * w * G;  // rank q's block at column q*w
-    if (G > 1 && (rc = peer_setup(h, api, ybytes))) return rc;
+    if (G > 1 && (rc = peer_setup(h, co, ybytes))) return rc;
     const bool p2p = G > 1 && h->p2p_state == 1;
     Carve cv;
     const size_t oofs = omega_mode == IDK_OMEGA_VERBATIM ? 0 : cv.take(sizeof(double) * l * m);
@@ -1781,9 +1889,7 @@ int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, 
         // barrier (a one-int NCCL all-reduce) tells each rank its Y is complete.  A
         // first barrier keeps this call's stores out of a peer's Y until that
         // peer's previous call (whose CPQR factors its Y in place) is done.
-        const idk::ncclResult_t pr =
-            api->AllReduce(h->d_flag, h->d_flag + 1, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
-        if (pr != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllReduce (barrier): ") + api->GetErrorString(pr));
+        if ((rc = co.barrier())) return rc;
         if (nr > 0) {
             idk::FanOut f;
             f.count = G;
@@ -1795,19 +1901,14 @@ int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, 
                                              h->stream));
             h->launches += 2;
         }
-        const idk::ncclResult_t br =
-            api->AllReduce(h->d_flag, h->d_flag + 1, 1, idk::kNcclInt32, idk::kNcclMin, h->nccl_comm, h->stream);
-        if (br != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllReduce (barrier): ") + api->GetErrorString(br));
+        if ((rc = co.barrier())) return rc;
     } else if (nr > 0) {  // this rank's columns of Y = Omega M, straight into its slot of the gathered Y
         IDK_CUDA(idk::sketch_gemm(omega, l, d_a_local, lda, trans, Y + b * l, l, static_cast<int>(l), nr, m, splits,
                                   splits > 1 ? reinterpret_cast<double*>(h->ws + pofs) : nullptr, h->stream));
         h->launches += splits > 1 ? 2 : 1;
     }
-    if (G > 1 && !p2p) {
-        const idk::ncclResult_t nr_ = api->AllGather(Y + static_cast<int64_t>(r) * w * l, Y, static_cast<size_t>(w * l),
-                                                    idk::kNcclFloat64, h->nccl_comm, h->stream);
-        if (nr_ != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclAllGather: ") + api->GetErrorString(nr_));
-    }
+    if (G > 1 && !p2p && (rc = co.allgather(Y + static_cast<int64_t>(r) * w * l, Y, sizeof(double) * w * l)))
+        return rc;
     // replicated deterministic CPQR: bit-identical on every rank, so no broadcast of the pivots
     long long* pos = reinterpret_cast<long long*>(h->ws + ws.pos);
     long long* piv = reinterpret_cast<long long*>(h->ws + ws.pivots);
@@ -1829,16 +1930,9 @@ int idk_id_sharded(idk_handle h, const double* d_a_local, int64_t m, int64_t n, 
     if (*h->h_status != 0x7f7f7f7f)
         return set_err(h, IDK_ERR_SINGULAR, "solve_triangular: zero diagonal at index " + std::to_string(*h->h_status));
     if (d_c && G > 1) {  // each column of C comes from its one owner: exact, no reduction
-        for (int64_t j0 = 0; j0 < k; j0 += 512) {
-            api->GroupStart();
-            for (int64_t j = j0; j < std::min<int64_t>(k, j0 + 512); ++j) {
-                double* col = d_c + j * m;
-                api->Broadcast(col, col, static_cast<size_t>(m), idk::kNcclFloat64, static_cast<int>(hcols[j] / w),
-                               h->nccl_comm, h->stream);
-            }
-            const idk::ncclResult_t gr = api->GroupEnd();
-            if (gr != 0) return set_err(h, IDK_ERR_NCCL, std::string("ncclBroadcast: ") + api->GetErrorString(gr));
-        }
+        std::vector<int> owner(static_cast<size_t>(k));
+        for (int64_t j = 0; j < k; ++j) owner[j] = static_cast<int>(hcols[j] / w);
+        if ((rc = co.columns_from_owners(d_c, m, k, owner))) return rc;
         IDK_CUDA(cudaStreamSynchronize(h->stream));
     }
     return IDK_OK;

@@ -155,6 +155,33 @@ class Context:
         self.check(self.lib.idk_comm_init(self.h, nranks, rank, buf))
         self.nranks, self.rank = nranks, rank
 
+    # idk_host_collectives callbacks: allgather(ctx, send, recv, bytes), broadcast(ctx, buf, bytes, root), barrier(ctx)
+    _AG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+    _BC = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int)
+    _BR = C.CFUNCTYPE(C.c_int, C.c_void_p)
+
+    class _HostColl(C.Structure):
+        _fields_ = [("ctx", C.c_void_p), ("allgather", C.c_void_p), ("broadcast", C.c_void_p), ("barrier", C.c_void_p)]
+
+    def set_host_collectives(self, nranks: int, rank: int, allgather, broadcast, barrier):
+        """A caller transport instead of NCCL (idk_set_host_collectives): Python
+        callables over host buffers -- allgather(send_addr, recv_addr, nbytes),
+        broadcast(buf_addr, nbytes, root), barrier(); raise to fail."""
+        def wrap(fn):
+            def cb(*args):
+                try:
+                    fn(*args[1:])
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+                    return 1
+            return cb
+        self._hc_refs = (self._AG(wrap(allgather)), self._BC(wrap(broadcast)), self._BR(wrap(barrier)))
+        st = self._HostColl(None, C.cast(self._hc_refs[0], C.c_void_p), C.cast(self._hc_refs[1], C.c_void_p),
+                            C.cast(self._hc_refs[2], C.c_void_p))
+        self._hc_struct = st
+        self.check(self.lib.idk_set_host_collectives(self.h, nranks, rank, C.byref(st)))
+        self.nranks, self.rank = nranks, rank
+
     def comm_destroy(self):
         self.check(self.lib.idk_comm_destroy(self.h))
         self.nranks, self.rank = 1, 0

@@ -134,6 +134,34 @@ def nccl_setup(device: int, group=None):
     return ctx
 
 
+def host_collectives_setup(device: int, group=None):
+    """Give this rank's C-ABI context host collectives over the torch.distributed
+    group (any backend, e.g. gloo on CPU) instead of NCCL: the transport for
+    setups without NCCL, and how the multi-rank C-ABI path is tested with
+    several processes on one GPU (tests/test_gpu_sharded_capi.py)."""
+    import ctypes as C
+    from . import idkit
+    world, rank = world_rank(group)
+    ctx = idkit.context(device)
+
+    def allgather(send, recv, nbytes):
+        src = torch.frombuffer((C.c_char * nbytes).from_address(send), dtype=torch.uint8).clone()
+        out = torch.empty(world * nbytes, dtype=torch.uint8)
+        dist.all_gather_into_tensor(out, src, group=group)
+        C.memmove(recv, out.data_ptr(), world * nbytes)
+
+    def broadcast(buf, nbytes, root):
+        t = torch.frombuffer((C.c_char * nbytes).from_address(buf), dtype=torch.uint8).clone()
+        dist.broadcast(t, src=root, group=group)
+        C.memmove(buf, t.data_ptr(), nbytes)
+
+    def barrier():
+        dist.barrier(group=group)
+
+    ctx.set_host_collectives(world, rank, allgather, broadcast, barrier)
+    return ctx
+
+
 def id_sharded_nccl(a_local: torch.Tensor, n_total: int, k: int, p: int, seed: int = 0, transposed: bool = False):
     """The product path: sketch -> in-place ncclAllGather(Y) -> replicated CPQR ->
     local Z -> owner broadcasts of C, all inside idk_id_sharded (call nccl_setup once)."""
