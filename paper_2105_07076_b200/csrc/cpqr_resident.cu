@@ -54,7 +54,7 @@ namespace idk {
 // (payload32 << 32 | tag32; aligned 64-bit stores are single-copy atomic), so
 // polling the G records is the barrier; cluster mode keeps records in shared
 // memory behind barrier.cluster.
-constexpr int kHdr = 4;
+constexpr int kHdr = 6;  // grid slot header: col, tau, beta, scale, ready flag (epoch | tag), pad
 constexpr int kCHdr = 6;  // cluster slot header: col, tau, beta, scale, vmax, pos
 constexpr int kRecWords = 4;  // vmax hi | vmax lo | pos | pad
 // Copies of each published grid-mode column: after the records every CTA reads
@@ -81,6 +81,7 @@ struct ResidentArgs {
     unsigned* barrier;        // debug: optional grid barrier before each exchange
     long long* trace;         // optional: %globaltimer at 8 phase marks per step, every CTA
     int push;                 // cluster: 1 = every CTA holds every candidate (push), 0 = headers only (pull)
+    unsigned long long epoch; // grid slot ready flags: per-launch epoch << 32 | exchange tag
 };
 
 namespace {
@@ -187,6 +188,14 @@ __device__ __forceinline__ void st_relaxed_v2(unsigned long long* p, unsigned lo
     asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long a) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void ld_relaxed_v2(const unsigned long long* p, unsigned long long& a,
                                               unsigned long long& b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
@@ -848,9 +857,12 @@ cpqr_resident_kernel(ResidentArgs a) {
                 for (int i = first + tid; i < l0; i += T) slot_copy(dst, cp)[kHdr + i - first] = cr[i];
         }
         __syncthreads();
+        if (tid < kColCopies) {
+            __threadfence();  // slot data before its ready flag (release)
+            if (have) st_relaxed_u64(reinterpret_cast<unsigned long long*>(slot_copy(dst, tid) + 4), a.epoch | tag);
+        }
         if (tid == 0) {
             const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
-            __threadfence();  // slot data before the tagged record (release)
             const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
             unsigned long long* rp = a.rec + (static_cast<size_t>(slot) * G + me) * kRecWords;
             st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
@@ -895,8 +907,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             s_rv[g] = vv;
             s_rp[g] = pp;
         }
-        if (tid < G) __threadfence();  // acquire: slot data after the records
-        __syncthreads();
+        __syncthreads();  // records are self-contained; the slot is acquired through its ready flag
         trace(step, 4);
         // every warp reduces the G records from shared memory (identical
         // result everywhere): no second CTA barrier before the column copy
@@ -967,6 +978,12 @@ cpqr_resident_kernel(ResidentArgs a) {
         trace(step, 5);
         // All threads: header + winner's column (one round trip), scaled into xbuf by absolute row.
         const double* src = slot_copy(slot_ptr(slot, gsel), me % kColCopies);
+        {  // the winner published its record before its column: wait for the column's ready flag
+            const unsigned long long want = a.epoch | tag;
+            const unsigned long long* fp = reinterpret_cast<const unsigned long long*>(src + 4);
+            while (ld_acquire_u64(fp) != want) {
+            }
+        }
         const double h0 = __ldcg(src);
         const double tu = __ldcg(src + 1);
         const double be = __ldcg(src + 2);
@@ -1002,6 +1019,16 @@ cpqr_resident_kernel(ResidentArgs a) {
         if (pubwarp) {
             double* dst = slot_ptr(parity, me);
             double* xscr = xpull;  // scratch (grid mode keeps the current reflector in xbuf)
+            // the record first: the global reduction needs only (norm, position), so it
+            // runs while this warp builds the candidate column; readers wait for the
+            // column's ready flag (written after a release fence) only for the winner
+            if (lane == 0) {
+                const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
+                const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
+                unsigned long long* rp = a.rec + (static_cast<size_t>(parity) * G + me) * kRecWords;
+                st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
+                st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
+            }
             if (have) {
                 const int wl0 = (winlc * S) & 31;
                 const double ww = __shfl_sync(kFull, todo ? wpend : 0.0, wl0);  // 0: already current
@@ -1034,15 +1061,10 @@ cpqr_resident_kernel(ResidentArgs a) {
                     dc[2] = be;
                     dc[3] = sc;
                 }
-            }
-            __threadfence();  // slot data before the tagged record (release)
-            __syncwarp();
-            if (lane == 0) {
-                const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
-                const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
-                unsigned long long* rp = a.rec + (static_cast<size_t>(parity) * G + me) * kRecWords;
-                st_relaxed_v2(rp, tagged(static_cast<unsigned>(vb >> 32), tag), tagged(static_cast<unsigned>(vb), tag));
-                st_relaxed_v2(rp + 2, tagged(pos32, tag), 0ull);
+                __threadfence();  // the column before its ready flag (release)
+                __syncwarp();
+                if (lane < kColCopies)
+                    st_relaxed_u64(reinterpret_cast<unsigned long long*>(slot_copy(dst, lane) + 4), a.epoch | tag);
             }
             trace_by(lane == 0, step, 3);
             asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
@@ -1366,6 +1388,8 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
     a.slots = reinterpret_cast<double*>(e + sizeof(unsigned long long) * kRecWords * 3 * G);
     a.trace = g_trace;
     a.push = p.push ? 1 : 0;
+    static unsigned long long launch_epoch = 0;  // grid slot flags of an earlier launch never match
+    a.epoch = (++launch_epoch) << 32;
     void* args[] = {&a};
     if (p.cluster) {
         void* fn = pick_kernel<true>(p.S, p.R);
