@@ -218,14 +218,15 @@ int check_cpqr_fits(idk_context* h, int64_t mrows, int64_t n, const CpqrChoice& 
 }
 
 cudaError_t run_cpqr(idk_context* h, const CpqrChoice& ch, double* W, int64_t mrows, int64_t n, int64_t k, char* base,
-                     const CpqrWs& w, int64_t ldw = 0) {
+                     const CpqrWs& w, int64_t ldw = 0, const double* Win = nullptr, int64_t ldin = 0) {
     if (ldw < mrows) ldw = mrows;
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     double* taus = reinterpret_cast<double*>(base + w.taus);
     if (ch.resident)
         return idk::cpqr_resident_launch(ch.plan, W, ldw, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv,
-                                         taus, base + w.pub, reinterpret_cast<unsigned*>(base + w.barrier), h->stream);
+                                         taus, base + w.pub, reinterpret_cast<unsigned*>(base + w.barrier), h->stream,
+                                         Win, ldin);
     return idk::cpqr_launch(W, ldw, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
                             reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream,
                             w.has_xg ? reinterpret_cast<double*>(base + w.xg) : nullptr);
@@ -234,13 +235,13 @@ cudaError_t run_cpqr(idk_context* h, const CpqrChoice& ch, double* W, int64_t mr
 // CPQR(W) -> Z, C, cols; W is m' x n (ld m'), already resident and mutable.
 int factor_and_solve(idk_context* h, const CpqrChoice& ch, double* W, int64_t mrows, int64_t n, int64_t k, char* base,
                      const CpqrWs& w, const double* d_a, int64_t lda, int64_t m_out, bool rows_of_a, int64_t* d_cols,
-                     double* d_z, double* d_c, bool det) {
+                     double* d_z, double* d_c, bool det, const double* Win = nullptr, int64_t ldin = 0) {
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     int* status = reinterpret_cast<int*>(base + w.status);
     IDK_CUDA(cudaMemsetAsync(status, 0x7f, sizeof(int), h->stream));
     mark(h, 2);
-    IDK_CUDA(run_cpqr(h, ch, W, mrows, n, k, base, w));
+    IDK_CUDA(run_cpqr(h, ch, W, mrows, n, k, base, w, mrows, Win, ldin));
     mark(h, 3);
     IDK_CUDA(idk::id_solve_z(W, mrows, static_cast<int>(k), 0, n, piv, pos, reinterpret_cast<double*>(base + w.r11),
                              status, d_z, h->stream));
@@ -285,15 +286,18 @@ int det_id(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda,
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     double* W = reinterpret_cast<double*>(h->ws + wofs);
     mark(h, 0);
+    // the resident CPQR reads A itself once and writes the factor to W: no working copy
+    const bool direct = !trans && ch.resident;
     if (trans) {
         IDK_CUDA(idk::transpose_copy(d_a, lda, n, m, W, m, h->stream));
         h->launches += 1;
-    } else {
+    } else if (!direct) {
         IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
                                    cudaMemcpyDeviceToDevice, h->stream));
     }
     mark(h, 1);
-    return factor_and_solve(h, ch, W, m, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, true);
+    return factor_and_solve(h, ch, W, m, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, true,
+                            direct ? d_a : nullptr, lda);
 }
 
 // Reference Box-Muller over mt19937_64 (random.cpp:10-15), column-major fill
@@ -910,12 +914,13 @@ int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n,
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     char* base = h->ws;
     double* W = reinterpret_cast<double*>(base + wofs);
-    IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
-                               cudaMemcpyDeviceToDevice, h->stream));
+    if (!ch.resident)  // the streaming kernel factors in place; the resident one reads A directly
+        IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
+                                   cudaMemcpyDeviceToDevice, h->stream));
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     double* taus = reinterpret_cast<double*>(base + w.taus);
-    IDK_CUDA(run_cpqr(h, ch, W, m, n, steps, base, w));
+    IDK_CUDA(run_cpqr(h, ch, W, m, n, steps, base, w, m, ch.resident ? d_a : nullptr, lda));
     long long* perm = d_perm ? reinterpret_cast<long long*>(d_perm) : reinterpret_cast<long long*>(base + permofs);
     IDK_CUDA(idk::cpqr_finish(W, m, static_cast<int>(m), n, static_cast<int>(steps), pos, piv, taus, perm, d_r, d_q,
                               h->stream));

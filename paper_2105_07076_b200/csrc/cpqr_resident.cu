@@ -66,6 +66,8 @@ constexpr int kColCopies = 4;
 struct ResidentArgs {
     double* W;
     int64_t ldw;
+    const double* Win;  // the matrix read once at the start (W itself, or the caller's A: no working copy)
+    int64_t ldin;
     int m;
     int64_t n;
     int k;
@@ -336,12 +338,12 @@ cpqr_resident_kernel(ResidentArgs a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int i = l0 + q + S * r;
-        yr[r] = (active && i < m) ? W[col * a.ldw + i] : 0.0;
+        yr[r] = (active && i < m) ? a.Win[col * a.ldin + i] : 0.0;
         part = fma(yr[r], yr[r], part);
     }
     for (int r = 0; r < nsr; ++r) {
         const int i = q + S * r;
-        const double v = active ? W[col * a.ldw + i] : 0.0;
+        const double v = active ? a.Win[col * a.ldin + i] : 0.0;
         if (lc < nc) myrows[i] = v;
         part = fma(v, v, part);
     }
@@ -1369,10 +1371,12 @@ size_t cpqr_resident_exchange_bytes(const ResidentPlan& p, int m) {
 
 cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, int m, int64_t n, int k,
                                  long long* pos_out, long long* pivots, double* taus, void* exch, unsigned* barrier,
-                                 cudaStream_t stream) {
+                                 cudaStream_t stream, const double* Win, int64_t ldin) {
     ResidentArgs a;
     a.W = W;
     a.ldw = ldw;
+    a.Win = Win ? Win : W;
+    a.ldin = Win ? ldin : ldw;
     a.m = m;
     a.n = n;
     a.k = k;

@@ -70,9 +70,11 @@ struct ResidentPlan {
 ResidentPlan cpqr_resident_plan(int m, int64_t n, int k, int num_sms, int cluster_pref);
 void cpqr_resident_set_trace(long long* device_buf);  // debug phase timing (nullptr = off)
 size_t cpqr_resident_exchange_bytes(const ResidentPlan& p, int m);
+// Win (optional): read the input from here (ld = ldin) instead of W, so W need
+// not hold a working copy first; the factor is written to W.
 cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, int m, int64_t n, int k,
                                  long long* pos_out, long long* pivots, double* taus, void* exch, unsigned* barrier,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, const double* Win = nullptr, int64_t ldin = 0);
 
 // trsm.cu
 int id_trsm_nb(int k);
