@@ -72,16 +72,15 @@ struct SmemT {
     static constexpr size_t BYTES = sizeof(double) * STAGE * kStagesT + 1024;  // + alignment slack
 };
 
-template <int WM, bool kNT>
-__global__ void __launch_bounds__(kThreadsT)
-sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  double* __restrict__ C, int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K,
-                  int64_t k_per_split) {
+// One CTA tile with WMA <= WM live 16-row boxes (the shared-memory layout is
+// WM's): the last M tile of cfg4 (l = 272 in 3 x 96 rows) has a box of pure
+// padding, which is neither loaded nor multiplied.
+template <int WMA, int WM, bool kNT>
+__device__ __forceinline__ void sketch_tile(const CUtensorMap& tmA, const CUtensorMap& tmB, double* __restrict__ C,
+                                            int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K,
+                                            int64_t k_per_split, double* smem, uint64_t* full) {
     using S = SmemT<WM>;
     constexpr int BM = S::BM;
-    extern __shared__ __align__(1024) double smem_raw[];
-    double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full[kStagesT];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
@@ -92,15 +91,7 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
     const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBKT - 1) / kBKT) : 0;
     C += static_cast<int64_t>(blockIdx.z) * split_stride;
 
-    if (tid == 0) {
-        for (int s = 0; s < kStagesT; ++s) mbar_init_t(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    }
-    __syncthreads();
-
-    constexpr unsigned kStageBytes = static_cast<unsigned>(sizeof(double) * S::STAGE);
+    constexpr unsigned kStageBytes = static_cast<unsigned>(sizeof(double) * (WMA * 256 + S::B_ELEMS));
     auto issue = [&](int kt) {  // thread 0 only
         const int st = kt % kStagesT;
         double* As = smem + st * S::STAGE;
@@ -108,7 +99,7 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         const int k0 = static_cast<int>(kbeg) + kt * kBKT;
         mbar_expect_tx_t(&full[st], kStageBytes);
 #pragma unroll
-        for (int g = 0; g < WM; ++g) tma_load_2d(As + g * 256, &tmA, m0 + 16 * g, k0, &full[st]);
+        for (int g = 0; g < WMA; ++g) tma_load_2d(As + g * 256, &tmA, m0 + 16 * g, k0, &full[st]);
         if constexpr (kNT) {
 #pragma unroll
             for (int b = 0; b < kBNT / 16; ++b) tma_load_2d(Bs + b * 256, &tmB, n0 + 16 * b, k0, &full[st]);
@@ -117,9 +108,9 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         }
     };
 
-    double acc[WM][4][2];
+    double acc[WMA][4][2];
 #pragma unroll
-    for (int a = 0; a < WM; ++a)
+    for (int a = 0; a < WMA; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
@@ -153,10 +144,10 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
         const double* Bs = As + S::A_ELEMS;
 #pragma unroll
         for (int kq = 0; kq < kBKT / 4; ++kq) {
-            double af[WM], bf[4];
+            double af[WMA], bf[4];
             const int ay = (kq & 1) ? yb : ya;
 #pragma unroll
-            for (int tm = 0; tm < WM; ++tm) af[tm] = As[tm * 256 + kq * 64 + ay];
+            for (int tm = 0; tm < WMA; ++tm) af[tm] = As[tm * 256 + kq * 64 + ay];
 #pragma unroll
             for (int tn = 0; tn < 4; ++tn) {
                 if constexpr (kNT) {
@@ -169,14 +160,14 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
                 }
             }
 #pragma unroll
-            for (int tm = 0; tm < WM; ++tm)
+            for (int tm = 0; tm < WMA; ++tm)
 #pragma unroll
                 for (int tn = 0; tn < 4; ++tn) dmma(acc[tm][tn], af[tm], bf[tn]);
         }
     }
 
 #pragma unroll
-    for (int tm = 0; tm < WM; ++tm) {
+    for (int tm = 0; tm < WMA; ++tm) {
         const int i = m0 + 16 * tm + 8 * wm + fr;
         if (i >= M) continue;
 #pragma unroll
@@ -186,6 +177,30 @@ sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
             if (j + 1 < N) C[(j + 1) * ldc + i] = acc[tm][tn][1];
         }
     }
+}
+
+template <int WM, bool kNT>
+__global__ void __launch_bounds__(kThreadsT)
+sketch_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  double* __restrict__ C, int64_t ldc, int64_t split_stride, int M, int64_t N, int64_t K,
+                  int64_t k_per_split) {
+    extern __shared__ __align__(1024) double smem_raw[];
+    double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kStagesT];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesT; ++s) mbar_init_t(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    __syncthreads();
+    if constexpr (WM > 2) {
+        if (static_cast<int>(blockIdx.x) * 16 * WM + 16 * (WM - 1) >= M) {  // last tile, last box all padding
+            sketch_tile<WM - 1, WM, kNT>(tmA, tmB, C, ldc, split_stride, M, N, K, k_per_split, smem, full);
+            return;
+        }
+    }
+    sketch_tile<WM, WM, kNT>(tmA, tmB, C, ldc, split_stride, M, N, K, k_per_split, smem, full);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
