@@ -418,6 +418,11 @@ int sketch_gemm_pick_splits(int M, int64_t N, int64_t K, int num_sms) {
     const int64_t tiles = ((M + 16 * wm - 1) / (16 * wm)) * ((N + kBN - 1) / kBN);
     int splits = 1;
     while (tiles * splits < 16LL * num_sms && K / (splits * 2) >= 256 && splits < 16) splits *= 2;
+    // long K ranges take one more doubling while each split keeps >= 128 k-tiles:
+    // more, shorter CTAs even out the wave tail (cfg4: 4 -> 8 splits, sketch
+    // 4.35 -> 4.29 ms; cfg5's 4096-long K stays at 4, where 8 was slower;
+    // profiles/sketch_padding_r02.txt)
+    if (tiles * splits < 32LL * num_sms && K / (splits * 2) >= 2048 && splits < 16) splits *= 2;
     return splits;
 }
 
