@@ -104,13 +104,22 @@ __device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
                  : "memory");
 }
 
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c[0]), "+d"(c[1])
                  : "d"(a), "d"(b));
 }
 
-template <int NBLK>
+// PAIRS: k and ldw even and 16-byte aligned bases -- operands move as 16-byte
+// pairs (cp.async.cg 16) and Z leaves as double2 stores: half the load/store
+// instructions, which at k <= 128 are half of the kernel's (ncu, cfg5).
+template <int NBLK, bool PAIRS>
 __global__ void __launch_bounds__(kDmmaThreads)
 id_trsm_dmma_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ R11, int k, int64_t n,
                     const long long* __restrict__ pos, double* __restrict__ Z) {
@@ -126,17 +135,41 @@ id_trsm_dmma_kernel(const double* __restrict__ W, int64_t ldw, const double* __r
     const int nb = static_cast<int>(min(static_cast<long long>(kDmmaNB), static_cast<long long>(n - c0)));
 
     // operands land by cp.async (all loads in flight at once); padding is written directly
-    for (int e = tid; e < KP * KP; e += kDmmaThreads) {
-        const int col = e / KP, row = e - col * KP;
-        double* dst = Rs + col * LD + row;
-        if (row < k && col < k) cp_async_8(dst, R11 + static_cast<int64_t>(col) * k + row);
-        else *dst = row == col ? 1.0 : 0.0;
-    }
-    for (int e = tid; e < kDmmaNB * KP; e += kDmmaThreads) {
-        const int c = e / KP, row = e - c * KP;
-        double* dst = Xs + c * LD + row;
-        if (c < nb && row < k) cp_async_8(dst, W + (c0 + c) * ldw + row);
-        else *dst = 0.0;
+    if constexpr (PAIRS) {
+        constexpr int KH = KP / 2;  // row pairs per column
+        for (int e = tid; e < KP * KH; e += kDmmaThreads) {
+            const int col = e / KH, row = 2 * (e - col * KH);
+            double* dst = Rs + col * LD + row;
+            if (row < k && col < k) {
+                cp_async_16(dst, R11 + static_cast<int64_t>(col) * k + row);
+            } else {
+                dst[0] = row == col ? 1.0 : 0.0;
+                dst[1] = row + 1 == col ? 1.0 : 0.0;
+            }
+        }
+        for (int e = tid; e < kDmmaNB * KH; e += kDmmaThreads) {
+            const int c = e / KH, row = 2 * (e - c * KH);
+            double* dst = Xs + c * LD + row;
+            if (c < nb && row < k) {
+                cp_async_16(dst, W + (c0 + c) * ldw + row);
+            } else {
+                dst[0] = 0.0;
+                dst[1] = 0.0;
+            }
+        }
+    } else {
+        for (int e = tid; e < KP * KP; e += kDmmaThreads) {
+            const int col = e / KP, row = e - col * KP;
+            double* dst = Rs + col * LD + row;
+            if (row < k && col < k) cp_async_8(dst, R11 + static_cast<int64_t>(col) * k + row);
+            else *dst = row == col ? 1.0 : 0.0;
+        }
+        for (int e = tid; e < kDmmaNB * KP; e += kDmmaThreads) {
+            const int c = e / KP, row = e - c * KP;
+            double* dst = Xs + c * LD + row;
+            if (c < nb && row < k) cp_async_8(dst, W + (c0 + c) * ldw + row);
+            else *dst = 0.0;
+        }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
@@ -199,7 +232,14 @@ id_trsm_dmma_kernel(const double* __restrict__ W, int64_t ldw, const double* __r
         const long long p = __shfl_sync(0xffffffffu, mp, t);
         if (c < nb) {
             const int64_t col = c0 + c;
-            for (int i = lane; i < k; i += 32) Z[col * k + i] = p < k ? (i == p ? 1.0 : 0.0) : Xs[c * LD + i];
+            if constexpr (PAIRS) {
+                double2* zc = reinterpret_cast<double2*>(Z + col * k);
+                const double2* xc = reinterpret_cast<const double2*>(Xs + c * LD);
+                for (int i2 = lane; i2 < k / 2; i2 += 32)
+                    zc[i2] = p < k ? make_double2(2 * i2 == p ? 1.0 : 0.0, 2 * i2 + 1 == p ? 1.0 : 0.0) : xc[i2];
+            } else {
+                for (int i = lane; i < k; i += 32) Z[col * k + i] = p < k ? (i == p ? 1.0 : 0.0) : Xs[c * LD + i];
+            }
         }
     }
 }
@@ -489,11 +529,15 @@ template <int NBLK>
 cudaError_t launch_trsm_dmma(const double* W, int64_t ldw, const double* R11, int k, int64_t n,
                              const long long* pos, double* Z, cudaStream_t stream) {
     const size_t smem = trsm_dmma_smem<NBLK>();
-    cudaError_t e = cudaFuncSetAttribute(id_trsm_dmma_kernel<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
     const int64_t blocks = (n + kDmmaNB - 1) / kDmmaNB;
-    id_trsm_dmma_kernel<NBLK><<<static_cast<unsigned>(blocks), kDmmaThreads, smem, stream>>>(W, ldw, R11, k, n, pos, Z);
+    const char* pv = getenv("IDK_TRSM_PAIRS");
+    const bool pairs = !(pv && atoi(pv) == 0) && k % 2 == 0 && ldw % 2 == 0 &&
+                       (reinterpret_cast<uintptr_t>(W) & 15) == 0 && (reinterpret_cast<uintptr_t>(R11) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(Z) & 15) == 0;
+    auto kern = pairs ? id_trsm_dmma_kernel<NBLK, true> : id_trsm_dmma_kernel<NBLK, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(blocks), kDmmaThreads, smem, stream>>>(W, ldw, R11, k, n, pos, Z);
     return cudaGetLastError();
 }
 
