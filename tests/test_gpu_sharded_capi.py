@@ -1,5 +1,5 @@
-"""The multi-rank C-ABI sharded path (idk_id_sharded) with several processes on
-one GPU: the ranks meet over gloo through idk_set_host_collectives (NCCL does
+"""The multi-rank C-ABI sharded path (idk_id_sharded) with 2, 3, 4 and 8
+processes on one GPU (SURVEY.md section 4 asks for G = 1, 2, 4, 8 on one box): the ranks meet over gloo through idk_set_host_collectives (NCCL does
 not allow two ranks on one device), and -- in peer mode -- map each other's Y
 buffers by CUDA IPC, so the fused sketch + all-gather (each rank's split-K
 reduction storing into every rank's Y) runs across processes.  No kernel waits
@@ -60,9 +60,9 @@ def _worker(rank, world, port, transposed, p2p, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("transposed", [False, True])
-@pytest.mark.parametrize("p2p", [True, False])
+@pytest.mark.parametrize("world,transposed,p2p", [(2, False, True), (2, True, True), (2, False, False),
+                                                  (2, True, False), (3, False, True), (3, True, False),
+                                                  (4, False, True), (4, True, True), (8, False, True)])
 def test_c_abi_sharded_multi_process(tmp_path, world, transposed, p2p):
     mp.spawn(_worker, args=(world, _free_port(), transposed, p2p, str(tmp_path)), nprocs=world, join=True)
     for r in range(world):
