@@ -174,7 +174,8 @@ IDK_API int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch,
  * (stride m*n), outputs packed as in the device entry.  Chunks of
  * 2 x num_SMs matrices are uploaded, factored and downloaded in a pipeline
  * (upload of chunk c+1 and download of chunk c-1 overlap the kernel of chunk
- * c); pinned host buffers make the copies asynchronous. */
+ * c); pinned host buffers make the copies asynchronous (with pageable buffers
+ * every copy is synchronous and the three stages run one after another). */
 IDK_API int idk_optim_id_batched_host(idk_handle h, const double* h_a, int64_t batch, int64_t m, int64_t n, int64_t k,
                                       int64_t* h_cols, double* h_z, double* h_c);
 
@@ -360,7 +361,7 @@ IDK_API int idk_matmul_ref(idk_handle h, const double* d_a, int64_t m, int64_t k
  * (host, ld = m), results into h_cols[i], h_z[i] (k * max(m, n)) and, if
  * h_c != NULL, h_c[i].  The upload of matrix i+1 and the download of result
  * i-1 overlap the compute of ID i on separate streams (pinned host buffers
- * make the copies asynchronous); statuses are checked once at the end, the
+ * make the copies asynchronous; pageable ones serialise the pipeline); statuses are checked once at the end, the
  * first failure is reported with its index. */
 IDK_API int idk_id_auto_host_many(idk_handle h, int64_t count, const double* const* h_a, int64_t m, int64_t n,
                                   int64_t k, int method, uint64_t seed, int64_t p, int omega_mode,
