@@ -159,7 +159,7 @@ def stage_rooflines(cfg, stage_avg, peaks, fp64_peak):
     stand-alone ncu numbers)."""
     work = stage_work(cfg, cfg.n)
     out = {"_note": "per-launch durations measured on each ID's lane stream while the other IDs in flight share "
-                    "the GPU: lower bounds of each kernel's own rate (stand-alone rates: profiles/ncu_full_r01.txt)"}
+                    "the GPU: lower bounds of each kernel's own rate (stand-alone rates: profiles/ncu_full_r02.json, launches_cfg4_r02.txt)"}
     for st, ms in stage_avg.items():
         if ms <= 0 or st not in work:
             continue
@@ -174,33 +174,63 @@ def stage_rooflines(cfg, stage_avg, peaks, fp64_peak):
                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gb / peaks["hbm_gbs"], "avg_launch_ms": ms}
             if st == "cpqr":
                 out[st]["per_pivot_step_us"] = 1e3 * ms / cfg.k
-        out[st]["kernel"] = stage_kernels(cfg).get(st, st)
+        out[st]["kernel"] = stage_kernels(cfg, cpqr_plan_for(cfg)).get(st, st)
     return out
 
 
-def stage_kernels(cfg):
-    """The kernels each stage launches for this config (what actually runs)."""
+def stage_kernels(cfg, plan=None):
+    """The kernels each stage launches for this config (what actually runs:
+    the dispatch of id_solve_z in csrc/trsm.cu and, for the CPQR, the plan the
+    library reports through idk_cpqr_plan)."""
     tall = cfg.m > cfg.n
     k = cfg.k
+    nblk = (k + 31) // 32
     if k <= 128:
-        trsm = f"id_trsm_dmma_kernel<{(k + 31) // 32}>"
+        trsm = f"id_trsm_dmma_kernel<{nblk}, 1>"
     elif k <= 256:
-        trsm = f"id_trsm_dmma_big_kernel<{(k + 31) // 32}>"
+        trsm = f"invert_diag_blocks_kernel + id_trsm_dinv_kernel<{nblk}, 64, 256>"
     else:
         trsm = "id_trsm_rl_kernel"
+    kind = (plan or {}).get("kind")
+    if kind == "resident-grid":
+        cpqr = (f"cpqr_resident_kernel (grid exchange: {plan['ctas']} CTAs, one per SM, tagged L2 records; "
+                f"{plan['cols_per_cta']} columns x {plan['threads_per_col']} threads per CTA)")
+    elif kind in ("cluster", "cluster-pull"):
+        cpqr = (f"cpqr_resident_kernel (one {plan['ctas']}-CTA cluster, DSMEM exchange; "
+                f"{plan['cols_per_cta']} columns x {plan['threads_per_col']} threads per CTA)")
+    elif kind == "streaming":
+        cpqr = "cpqr_kernel (streaming, matrix in HBM)"
+    else:
+        cpqr = "cpqr_resident_kernel"
     return {
         "prep": "omega_philox_kernel" if cfg.randomized else ("transpose_kernel" if tall else "cudaMemcpy2DAsync"),
         "sketch": f"sketch_tma_kernel<WM, {'true' if tall else 'false'}> + splitk_reduce_kernel (TMA-fed DMMA m8n8k4)",
-        "cpqr": "cpqr_resident_kernel (on-chip CPQR; 16-CTA cluster DSMEM exchange or one CTA per SM grid exchange)",
+        "cpqr": cpqr,
         "solve": "gather_r11_kernel + " + trsm,
-        "gather": "gather_rows_kernel" if tall else "gather_columns_vec_kernel",
+        "gather": "gather_rows_kernel<2>" if tall else "gather_columns_vec_kernel",
         "batched": "batched_fast_kernel<64, 16>",
     }
 
 
+_PLAN = {}
+
+
+def cpqr_plan_for(cfg):
+    """idk_cpqr_plan of the CPQR this config runs (Y: l x n, or the dual's l x m)."""
+    if cfg.name not in _PLAN:
+        try:
+            import paper_2105_07076_b200 as idk
+            m, n = (cfg.n, cfg.m) if cfg.m > cfg.n else (cfg.m, cfg.n)
+            rows = cfg.l if cfg.randomized else m
+            _PLAN[cfg.name] = idk.context(0).cpqr_plan(rows, n, cfg.k)
+        except Exception:  # noqa: BLE001 - labels only
+            _PLAN[cfg.name] = None
+    return _PLAN[cfg.name]
+
+
 def roofline_for(stage, work, avg_ms, peaks, fp64_peak, traffic, cfg):
     secs = avg_ms / 1e3
-    kern = stage_kernels(cfg).get(stage, stage)
+    kern = stage_kernels(cfg, cpqr_plan_for(cfg)).get(stage, stage)
     if stage in ("sketch", "solve") and "flops" in work:
         achieved = work["flops"] / secs / 1e12
         return {"kernel": kern, "bound": "tensor", "achieved": achieved,
@@ -461,7 +491,10 @@ def run_ours(args):
     if stage_tot:
         stage_avg = {s_: v / n_stage for s_, v in stage_tot.items()}
         dom = max(stage_avg, key=stage_avg.get)
-        traffic = (ncu.get(cfg.name) or {}).get(dom, {}).get("dram_bytes_per_launch")
+        nc = ncu.get(cfg.name) or {}
+        traffic = nc.get(dom, {}).get("dram_bytes_per_launch")
+        if dom == "sketch" and traffic is not None and "splitk_reduce" in nc:
+            traffic += nc["splitk_reduce"]["dram_bytes_per_launch"]  # the stage's two kernels, as timed
         roofline = roofline_for(dom, stage_work(cfg, cfg.n)[dom], stage_avg[dom], peaks, fp64, traffic, cfg)
         # share of the device time per ID (with nb IDs in flight, per-launch times include co-running kernels)
         roofline["step_share"] = stage_avg[dom] / sum(stage_avg.values())
