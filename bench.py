@@ -208,7 +208,7 @@ def stage_kernels(cfg, plan=None):
         "cpqr": cpqr,
         "solve": "gather_r11_kernel + " + trsm,
         "gather": "gather_rows_kernel<2>" if tall else "gather_columns_vec_kernel",
-        "batched": "batched_fast_kernel<64, 16>",
+        "batched": "batched_group_kernel<64, 2, 16>",
     }
 
 

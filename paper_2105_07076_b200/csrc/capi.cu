@@ -769,7 +769,18 @@ int idk_optim_id_batched(idk_handle h, const double* d_a, int64_t batch, int64_t
         if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
         status = reinterpret_cast<int*>(h->ws + sofs);
     }
-    if (fast)
+    // two threads per column (batched_group.cu) by default: 3 % faster than one thread per column
+    // on cfg3 (profiles/batched_group_r02.txt); IDK_BATCHED_GROUP=0 selects batched_fast.cu
+    static const int group = [] {
+        const char* e = getenv("IDK_BATCHED_GROUP");
+        return e ? atoi(e) : 2;
+    }();
+    if (fast && group > 0 && idk::batched_group_ok(d_a, lda, stride, static_cast<int>(m), static_cast<int>(n),
+                                                   static_cast<int>(k), h->smem_optin))
+        IDK_CUDA(idk::batched_id_group(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n),
+                                       static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
+                                       h->num_sms, group, h->stream));
+    else if (fast)
         IDK_CUDA(idk::batched_id_fast(d_a, lda, stride, batch, static_cast<int>(m), static_cast<int>(n),
                                       static_cast<int>(k), reinterpret_cast<long long*>(d_cols), d_z, d_c, status,
                                       h->num_sms, h->stream));

@@ -101,6 +101,13 @@ bool batched_fast_ok(const double* A, int64_t lda, int64_t stride, int m, int n,
 cudaError_t batched_id_fast(const double* A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
                             long long* cols, double* Z, double* C, int* status, int num_sms, cudaStream_t stream);
 
+// batched_group.cu (S threads per column; group = 2 or 4)
+size_t batched_group_smem_bytes(int n, int k);
+bool batched_group_ok(const double* A, int64_t lda, int64_t stride, int m, int n, int k, size_t smem_optin);
+cudaError_t batched_id_group(const double* A, int64_t lda, int64_t stride, int64_t batch, int m, int n, int k,
+                             long long* cols, double* Z, double* C, int* status, int num_sms, int group,
+                             cudaStream_t stream);
+
 // ldlt.cu (optim_rid's symmetric-indefinite solve)
 size_t ldlt_scratch_bytes(int k);
 cudaError_t ldlt_factor(const double* S, int k, double* F, void* scratch, int* status, cudaStream_t stream);
