@@ -62,6 +62,7 @@ constexpr int kRecWords = 4;  // vmax hi | vmax lo | pos | pad
 // the same ~17 L2 lines; reader g reads copy g % kColCopies
 // (profiles/grid_exchange_r02.txt: cfg4 8.39 -> 7.53 us per step).
 constexpr int kColCopies = 4;
+constexpr int kPollWarps = 8;  // grid records reduced by their polling warps first (G <= 256)
 
 struct ResidentArgs {
     double* W;
@@ -284,6 +285,9 @@ cpqr_resident_kernel(ResidentArgs a) {
     __shared__ unsigned long long s_mbar[2];      // cluster: bulk-push barriers, one per slot parity
     __shared__ double s_rv[kCluster ? 1 : 160];  // grid: the G records of this exchange
     __shared__ unsigned s_rp[kCluster ? 1 : 160];
+    __shared__ double s_gv[kPollWarps];  // grid: per polling warp (max, lowest qualifying position, its CTA)
+    __shared__ unsigned s_gp[kPollWarps];
+    __shared__ unsigned s_gg[kPollWarps];
 
     const int tid = threadIdx.x, T = blockDim.x;
     const int lane = tid & 31, wid = tid >> 5, nw = T >> 5;
@@ -435,7 +439,7 @@ cpqr_resident_kernel(ResidentArgs a) {
     // runs while the exchange for the next pivot is in flight.
     bool todo = false;
     double wpend = 0.0;
-    int psr0 = 0, prr0 = 0;
+    int psr0 = 0;
     const double* pxa = xbuf;
     auto do_axpy = [&]() {
         if (!todo) return;
@@ -457,12 +461,10 @@ cpqr_resident_kernel(ResidentArgs a) {
             myrows[i] = fma(-w, pxa[i], myrows[i]);
         }
         // straight-line over every register row (all reflector loads in flight
-        // at once); retired rows keep their value bit for bit through a select
+        // at once); v is zero on retired rows, so they keep their value without a
+        // select (ncu: the select was 11 % of the kernel's instructions)
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const double nv = fma(-w, xr[S * r], yr[r]);
-            yr[r] = r >= prr0 ? nv : yr[r];
-        }
+        for (int r = 0; r < R; ++r) yr[r] = fma(-w, xr[S * r], yr[r]);
     };
 
     // ---------------- cluster exchange (push, then all-local select) ----------------
@@ -901,7 +903,13 @@ cpqr_resident_kernel(ResidentArgs a) {
 #endif
         int slot = parity;
         // every thread polls at most a few records, all in flight at once:
-        // one L2 round trip after the last arrival instead of one per record
+        // one L2 round trip after the last arrival instead of one per record.
+        // When every record has its own thread (T >= G), each polling warp also
+        // reduces its 32 records before the barrier, so afterwards a warp combines
+        // <= 8 warp records instead of all G (ncu: the G-record reduction in every
+        // warp was 16 % of the kernel's instructions); a near tie at either level
+        // falls back to the exact reduction over all records below.
+        const bool two_level = T >= G && G <= 32 * kPollWarps;
         for (int g = tid; g < G; g += T) {
             double vv;
             unsigned pp;
@@ -909,12 +917,41 @@ cpqr_resident_kernel(ResidentArgs a) {
             s_rv[g] = vv;
             s_rp[g] = pp;
         }
+        if (two_level && wid < (G + 31) / 32) {
+            const double vv = tid < G ? s_rv[tid] : -1.0;  // this thread's own record
+            const unsigned pp = tid < G ? s_rp[tid] : 0xffffffffu;
+            const double wm = warp_max_nonneg(vv);
+            const bool qu = vv >= 0.0 && qualifies(vv, wm);
+            const bool wamb = __any_sync(kFull, qu && vv != wm);
+            const unsigned wp = __reduce_min_sync(kFull, qu ? pp : 0xffffffffu);
+            const unsigned wg = __reduce_min_sync(kFull, (qu && pp == wp) ? static_cast<unsigned>(tid) : 0xffffffffu);
+            if (lane == 0) {
+                s_gv[wid] = wm;
+                s_gp[wid] = wp;
+                s_gg[wid] = wamb ? 0xfffffffeu : wg;
+            }
+        }
         __syncthreads();  // records are self-contained; the slot is acquired through its ready flag
         trace(step, 4);
+        int gsel = -1;
+        unsigned wsel = 0xffffffffu;
+        bool done = false;
+        if (two_level) {
+            const int npw = (G + 31) / 32;
+            const double v = lane < npw ? s_gv[lane] : -1.0;
+            const unsigned p = lane < npw ? s_gp[lane] : 0xffffffffu;
+            const unsigned gg = lane < npw ? s_gg[lane] : 0xffffffffu;
+            const double cmax = warp_max_nonneg(v);
+            const bool qu = v >= 0.0 && qualifies(v, cmax);
+            if (!__any_sync(kFull, (qu && v != cmax) || gg == 0xfffffffeu)) {
+                wsel = __reduce_min_sync(kFull, qu ? p : 0xffffffffu);
+                gsel = static_cast<int>(__reduce_min_sync(kFull, (qu && p == wsel) ? gg : 0xffffffffu));
+                done = wsel != 0xffffffffu;
+            }
+        }
+        if (!done)
         // every warp reduces the G records from shared memory (identical
         // result everywhere): no second CTA barrier before the column copy
-        int gsel;
-        unsigned wsel;
         {
             double v[kRecPerLane];
             unsigned p[kRecPerLane];
@@ -1178,7 +1215,6 @@ cpqr_resident_kernel(ResidentArgs a) {
                 const double w = mul_rn(group_sum<S>((d0 + d1) + (d2 + d3)), tau);
                 wpend = w;
                 psr0 = sr0;
-                prr0 = rr0;
                 pxa = xa;
                 todo = true;
                 head = ys - w;  // row s has v_0 = 1
