@@ -69,7 +69,13 @@ def recorded(*marks):
 pw = [("winner rows staged", 2, 8), ("pending update + norm", 8, 9), ("reflector scalars", 9, 10),
       ("scaled v + header", 10, 11), ("fence.proxy.async", 11, 12), ("bulk pushes issued", 12, 3)]
 for nm, a0, a1 in pw:
-    if recorded(a0, a1):
+    if recorded(a0, a1) and recorded(12):
+        d = t[:, :steps, a1] - t[:, :steps, a0]
+        print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
+# grid publish path of the publishing warp (marks 2 -> 8 -> 9 -> 10 -> 11 -> 3)
+if recorded(8, 9, 10, 11) and not recorded(12):
+    for nm, a0, a1 in [("rows staged", 2, 8), ("column to L2 + norm", 8, 9), ("reflector + header", 9, 10),
+                       ("release fence", 10, 11), ("ready flags", 11, 3)]:
         d = t[:, :steps, a1] - t[:, :steps, a0]
         print(f"  {nm:22s} {d[0].mean():9.0f} {d.mean():9.0f} {d.max(axis=0).mean():9.0f}")
 if recorded(4, 13, 14, 5):  # grid select: records -> vmax -> winner (before the tie pass) -> done
