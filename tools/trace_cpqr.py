@@ -89,6 +89,14 @@ rel3 = (t[:, :steps, 3] - t[:, :steps, 3].min(axis=0)).mean(axis=1)
 order = np.argsort(smid)
 print("per-CTA mean lateness (ns) of 'records read' / 'published', by SM id:")
 print("  " + " ".join(f"{int(smid[g])}:{rel4[g]:.0f}/{rel3[g]:.0f}" for g in order))
+# the same by CTA (block) index, with each CTA's own phase durations: is a late CTA slow in its own
+# update / argmax (marks 0 -> 2), or does it start late (mark 0 relative to the earliest CTA)?
+rel0 = (t[:, :steps, 0] - t[:, :steps, 0].min(axis=0)).mean(axis=1)
+upd = (t[:, :steps, 2] - t[:, :steps, 0]).mean(axis=1)
+pub = (t[:, :steps, 3] - t[:, :steps, 2]).mean(axis=1)
+print("per-CTA by block index: sm | start lateness | update+argmax | publish | 'published' lateness")
+for g in range(G):
+    print(f"  cta {g:3d} sm {int(smid[g]):3d}  {rel0[g]:6.0f} {upd[g]:6.0f} {pub[g]:6.0f} {rel3[g]:6.0f}")
 for lo, hi in [(0, 10), (k // 2 - 5, k // 2 + 5), (steps - 10, steps)]:
     dd = [(t[:, lo:hi, i + 1] - t[:, lo:hi, i]).mean() for i in range(6)]
     print(f"  steps {lo:3d}-{hi:3d}: " + " ".join(f"{x:7.0f}" for x in dd))
