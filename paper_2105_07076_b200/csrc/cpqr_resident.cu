@@ -224,6 +224,9 @@ __device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(unsigned a, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -282,14 +285,19 @@ cpqr_resident_kernel(ResidentArgs a) {
     __shared__ unsigned s_wl[32];
     __shared__ long long s_sel[3];  // grid tie pass: -, winning position, winning CTA
     __shared__ double s_help[kHelpWarps + 2];  // tall candidate build: partial norms, pending w, alpha
-    __shared__ unsigned long long s_mbar[2];      // cluster: bulk-push barriers, one per slot parity
+    __shared__ unsigned long long s_mbar[2];      // cluster: bulk-push barriers, one per slot parity;
+                                                  // grid: candidate handed to the publisher / consumed by it
+    __shared__ double s_pubw;                     // grid: the candidate's pending axpy weight
+    __shared__ int s_publc;                       // grid: the candidate's local column (-1: none)
     __shared__ double s_rv[kCluster ? 1 : 160];  // grid: the G records of this exchange
     __shared__ unsigned s_rp[kCluster ? 1 : 160];
     __shared__ double s_gv[kPollWarps];  // grid: per polling warp (max, lowest qualifying position, its CTA)
     __shared__ unsigned s_gp[kPollWarps];
     __shared__ unsigned s_gg[kPollWarps];
 
-    const int tid = threadIdx.x, T = blockDim.x;
+    // grid mode: the last warp only publishes the CTA's candidate (no columns); T counts the workers
+    const int tid = threadIdx.x, T = kCluster ? blockDim.x : blockDim.x - 32;
+    const bool publisher = !kCluster && tid >= T;
     const int lane = tid & 31, wid = tid >> 5, nw = T >> 5;
     const int lc = tid / S, q = tid % S;
     const int me = kCluster ? static_cast<int>(cg::this_cluster().block_rank()) : blockIdx.x;
@@ -302,6 +310,12 @@ cpqr_resident_kernel(ResidentArgs a) {
     double* myrows = rows + static_cast<size_t>(lc < nc ? lc : 0) * lds;
     const int gbase = lane & ~(S - 1);
     constexpr unsigned kFull = 0xffffffffu;
+
+    // barrier over the threads that own columns (grid mode: without the publisher warp)
+    auto cta_sync = [&]() {
+        if constexpr (kCluster) __syncthreads();
+        else asm volatile("bar.sync 3, %0;" ::"r"(T) : "memory");
+    };
 
     // phase marks (tools/trace_cpqr.py) exist only in builds with -DIDK_CPQR_TRACE:
     // the checks cost code size in the step loop, which the serial phases feel
@@ -331,6 +345,12 @@ cpqr_resident_kernel(ResidentArgs a) {
         if (tid == 0) {
             mbar_init(smem_u32(&s_mbar[0]), 1);
             mbar_init(smem_u32(&s_mbar[1]), 1);
+            fence_mbar_init();
+        }
+    } else {
+        if (tid == 0) {
+            mbar_init(smem_u32(&s_mbar[0]), 1);  // candidate staged (owner warp -> publisher)
+            mbar_init(smem_u32(&s_mbar[1]), 1);  // candidate consumed (publisher -> owner warp)
             fence_mbar_init();
         }
     }
@@ -395,7 +415,7 @@ cpqr_resident_kernel(ResidentArgs a) {
         const unsigned wm = __reduce_min_sync(kFull, key);
         const unsigned wl = __reduce_min_sync(kFull, (key == wm) ? static_cast<unsigned>(lc) : 0xffffffffu);
         if (lane == 0) red_l[wid] = static_cast<long long>((static_cast<unsigned long long>(wm) << 32) | wl);
-        __syncthreads();
+        cta_sync();
         const unsigned long long mine = lane < nw ? static_cast<unsigned long long>(red_l[lane]) : ~0ull;
         const unsigned best = __reduce_min_sync(kFull, static_cast<unsigned>(mine >> 32));
         winlc = static_cast<int>(__reduce_min_sync(
@@ -418,7 +438,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             s_wp[wid] = wp;
             s_wl[wid] = wl;
         }
-        __syncthreads();
+        cta_sync();
         const double v = lane < nw ? s_wv[lane] : -1.0;
         const unsigned p = lane < nw ? s_wp[lane] : 0xffffffffu;
         const unsigned l = lane < nw ? s_wl[lane] : 0xffffffffu;
@@ -860,7 +880,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             for (int cp = 0; cp < kColCopies; ++cp)
                 for (int i = first + tid; i < l0; i += T) slot_copy(dst, cp)[kHdr + i - first] = cr[i];
         }
-        __syncthreads();
+        cta_sync();
         if (tid < kColCopies) {
             __threadfence();  // slot data before its ready flag (release)
             if (have) st_relaxed_u64(reinterpret_cast<unsigned long long*>(slot_copy(dst, tid) + 4), a.epoch | tag);
@@ -931,7 +951,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                 s_gg[wid] = wamb ? 0xfffffffeu : wg;
             }
         }
-        __syncthreads();  // records are self-contained; the slot is acquired through its ready flag
+        cta_sync();  // records are self-contained; the slot is acquired through its ready flag
         trace(step, 4);
         int gsel = -1;
         unsigned wsel = 0xffffffffu;
@@ -1009,7 +1029,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                         s_sel[2] = g2;
                     }
                 }
-                __syncthreads();
+                cta_sync();
                 wsel = static_cast<unsigned>(s_sel[1]);
                 gsel = static_cast<int>(s_sel[2]);
             }
@@ -1035,7 +1055,7 @@ cpqr_resident_kernel(ResidentArgs a) {
             }
             xbuf[i] = x;
         }
-        __syncthreads();
+        cta_sync();
         piv = __double_as_longlong(h0);
         ppos = wsel;
         tau = tu;
@@ -1043,10 +1063,15 @@ cpqr_resident_kernel(ResidentArgs a) {
         xa = xbuf;
     };
 
-    // Grid round: as in cluster mode, the warp holding the CTA's winner builds
-    // the candidate's updated column with all 32 lanes (its deferred update
-    // applied to a raw copy), writes it to the L2 slot and releases the tagged
-    // record; the other warps apply their deferred axpy while the records fly.
+    // Grid round.  The warp holding the CTA's winner releases the tagged record, stages the
+    // winner's register rows and hands the candidate to the publisher warp, which builds the
+    // updated column with all 32 lanes (the winner's deferred update applied to the raw copy),
+    // writes it to the L2 slot and sets its ready flags.  The publisher owns no columns and
+    // takes no part in the workers' barriers, so no worker waits for the publish of its own
+    // CTA (trace before: the publishing warp reached the exchange barrier 3.3 us after the
+    // CTA argmax -- 2.4 us of publish plus its own axpy -- and every other warp waited there);
+    // only the owner warp waits until the publisher has read the candidate's shared rows
+    // before its axpy overwrites them.
     auto grid_round = [&](int first, bool cand, double lv, long long pos, int step) {
         int winpos, winlc;
         const double mx = cta_argmax(cand, lv, pos, winpos, winlc);
@@ -1054,13 +1079,12 @@ cpqr_resident_kernel(ResidentArgs a) {
         const int parity = first & 1;
         const unsigned tag = static_cast<unsigned>(first + 1);
         const bool have = winpos != INT_MAX;
-        const bool pubwarp = wid == (have ? (winlc * S) >> 5 : 0);
-        if (pubwarp) {
-            double* dst = slot_ptr(parity, me);
+        const bool ownwarp = wid == (have ? (winlc * S) >> 5 : 0);
+        if (ownwarp) {
             double* xscr = xpull;  // scratch (grid mode keeps the current reflector in xbuf)
             // the record first: the global reduction needs only (norm, position), so it
-            // runs while this warp builds the candidate column; readers wait for the
-            // column's ready flag (written after a release fence) only for the winner
+            // runs while the candidate column is built; readers wait for the column's
+            // ready flag (written after a release fence) only for the winner
             if (lane == 0) {
                 const unsigned pos32 = have ? static_cast<unsigned>(winpos) : 0xffffffffu;
                 const unsigned long long vb = static_cast<unsigned long long>(__double_as_longlong(mx));
@@ -1078,46 +1102,72 @@ cpqr_resident_kernel(ResidentArgs a) {
                         if (i >= first && i < m) xscr[i] = yr[r];
                     }
                 }
-                __syncwarp();
-                trace_by(lane == 0, step, 8);
-                const double* wrow = rows + static_cast<size_t>(winlc) * lds;
-                double al = 0.0, tl = 0.0;
-                for (int i = first + lane; i < m; i += 32) {
-                    const double y = fma(-ww, xa[i], i < l0 ? wrow[i] : xscr[i]);  // == the group's own axpy
-#pragma unroll
-                    for (int cp = 0; cp < kColCopies; ++cp) slot_copy(dst, cp)[kHdr + i - first] = y;
-                    if (i == first) al = y;
-                    else tl = fma(y, y, tl);
+                if (lane == 0) {
+                    s_pubw = ww;
+                    s_publc = winlc;
                 }
-                al = __shfl_sync(kFull, al, 0);
-                tl = warp_sum(tl);
-                trace_by(lane == 0, step, 9);
-                if (lane < kColCopies) {
-                    double tu, be, sc;
-                    reflector(al, tl, m - first, tu, be, sc);
-                    double* dc = slot_copy(dst, lane);
-                    dc[0] = __longlong_as_double(c0 + winlc);
-                    dc[1] = tu;
-                    dc[2] = be;
-                    dc[3] = sc;
-                }
-                trace_by(lane == 0, step, 10);
-                __threadfence();  // the column before its ready flag (release)
-                __syncwarp();
-                trace_by(lane == 0, step, 11);
-                if (lane < kColCopies)
-                    st_relaxed_u64(reinterpret_cast<unsigned long long*>(slot_copy(dst, lane) + 4), a.epoch | tag);
+            } else if (lane == 0) {
+                s_publc = -1;
             }
-            trace_by(lane == 0, step, 3);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s_mbar[0]));
+            trace_by(lane == 0, step, 8);
+            mbar_wait(smem_u32(&s_mbar[1]), static_cast<unsigned>(parity));  // candidate rows consumed
         }
-        // The other warps run their deferred axpy while this CTA's candidate is being
-        // published: only the publishing warp touches the candidate column's rows
-        // (cfg4 CPQR 1.682 -> 1.635 ms against waiting for the publish on named barrier 1).
         do_axpy();
         trace(step, 7);
         grid_exchange(parity, tag, first, cand, lv, pos, step);
     };
 
+    // The publisher warp's side of exchange `first`.
+    auto grid_publish = [&](int first) {
+        const int parity = first & 1;
+        const unsigned tag = static_cast<unsigned>(first + 1);
+        mbar_wait(smem_u32(&s_mbar[0]), static_cast<unsigned>(parity));
+        const int winlc = s_publc;
+        if (winlc >= 0) {
+            const double ww = s_pubw;
+            double* dst = slot_ptr(parity, me);
+            const double* xscr = xpull;
+            const double* wrow = rows + static_cast<size_t>(winlc) * lds;
+            double al = 0.0, tl = 0.0;
+            for (int i = first + lane; i < m; i += 32) {
+                const double y = fma(-ww, xbuf[i], i < l0 ? wrow[i] : xscr[i]);  // == the group's own axpy
+#pragma unroll
+                for (int cp = 0; cp < kColCopies; ++cp) slot_copy(dst, cp)[kHdr + i - first] = y;
+                if (i == first) al = y;
+                else tl = fma(y, y, tl);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s_mbar[1]));  // shared rows, scratch and reflector read
+            al = __shfl_sync(kFull, al, 0);
+            tl = warp_sum(tl);
+            trace_by(lane == 0, first - 1, 9);
+            if (lane < kColCopies) {
+                double tu, be, sc;
+                reflector(al, tl, m - first, tu, be, sc);
+                double* dc = slot_copy(dst, lane);
+                dc[0] = __longlong_as_double(c0 + winlc);
+                dc[1] = tu;
+                dc[2] = be;
+                dc[3] = sc;
+            }
+            trace_by(lane == 0, first - 1, 10);
+            __threadfence();  // the column before its ready flag (release)
+            __syncwarp();
+            trace_by(lane == 0, first - 1, 11);
+            if (lane < kColCopies)
+                st_relaxed_u64(reinterpret_cast<unsigned long long*>(slot_copy(dst, lane) + 4), a.epoch | tag);
+        } else if (lane == 0) {
+            mbar_arrive(smem_u32(&s_mbar[1]));
+        }
+        trace_by(lane == 0, first - 1, 3);
+    };
+
+    if (publisher) {
+        if constexpr (!kCluster)
+            for (int first = 0; first < a.k; ++first) grid_publish(first);
+    } else {
     // ---- pivot 0 ----
     {
         const bool cand = active && q == 0;
@@ -1263,6 +1313,7 @@ cpqr_resident_kernel(ResidentArgs a) {
         else grid_round(s + 1, cand, lv, mypos, s);
         trace(s, 6);
     }
+    }  // workers
 
     do_axpy();
     // ---- write back (the only write of W) ----
@@ -1313,7 +1364,8 @@ ResidentPlan plan_for(int m, int64_t n, int k, int G_target, bool cluster, size_
     static const int Rs[2] = {32, 16};
     static const int Ss[6] = {32, 16, 8, 4, 2, 1};
     for (int R : Rs) {
-        const int maxT = R >= 32 ? 512 : (R >= 16 ? 640 : 768);
+        // grid mode adds the publisher warp to the launch (the launch bound counts it)
+        const int maxT = (R >= 32 ? 512 : (R >= 16 ? 640 : 768)) - (cluster ? 0 : 32);
         for (int S : Ss) {
             const int threads = ((S * nc + 31) / 32) * 32;
             if (threads > maxT || threads < 32) continue;
@@ -1467,7 +1519,7 @@ cudaError_t cpqr_resident_launch(const ResidentPlan& p, double* W, int64_t ldw, 
         err = cudaMemsetAsync(barrier, 0, sizeof(unsigned), stream);
         if (err != cudaSuccess) return err;
     }
-    return cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(p.threads), args, p.smem, stream);
+    return cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(p.threads + 32), args, p.smem, stream);  // + the publisher warp
 }
 
 }  // namespace idk
