@@ -1097,10 +1097,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                 const double ww = __shfl_sync(kFull, todo ? wpend : 0.0, wl0);  // 0: already current
                 if (lc == winlc) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int i = l0 + q + S * r;
-                        if (i >= first && i < m) xscr[i] = yr[r];
-                    }
+                    for (int r = 0; r < R; ++r) xscr[l0 + q + S * r] = yr[r];  // retired / padding rows too: the scratch covers them
                 }
                 if (lane == 0) {
                     s_pubw = ww;
