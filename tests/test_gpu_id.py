@@ -432,3 +432,31 @@ def test_batched_host_entry_matches_device_entry(idk, oracle):
     bad[650] = 0.0
     with pytest.raises(idk.NotPositiveDefiniteError, match="matrix 650"):
         idk.optim_id_batched(bad, 16)
+
+
+def test_batched_kernel_variants_agree(tmp_path):
+    """IDK_BATCHED_GROUP selects the batched ID kernel when the library first runs one: the
+    default (two threads per column, batched_group.cu) and 0 (one thread per column,
+    batched_fast.cu) must pick the same columns and agree on Z within rounding."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "run_batched.py"
+    script.write_text(
+        "import sys, numpy as np, torch\n"
+        "sys.path.insert(0, %r)\n"
+        "import paper_2105_07076_b200 as idk\n"
+        "from paper_2105_07076_b200.configs import low_rank_batch_np\n"
+        "a = low_rank_batch_np(150, 64, 256, 16, 1e-4, 11)\n"
+        "cols, z, c = idk.optim_id_batched(torch.from_numpy(a).cuda(), 16)\n"
+        "np.savez(sys.argv[1], cols=cols.cpu().numpy(), z=z.cpu().numpy(), c=c.cpu().numpy())\n"
+        % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = {}
+    for g in ("0", "2"):
+        env = dict(os.environ, IDK_BATCHED_GROUP=g)
+        path = tmp_path / f"out{g}.npz"
+        subprocess.run([sys.executable, str(script), str(path)], check=True, env=env, timeout=600)
+        out[g] = np.load(path)
+    assert np.array_equal(out["0"]["cols"], out["2"]["cols"])
+    assert np.array_equal(out["0"]["c"], out["2"]["c"])
+    assert rel(out["0"]["z"], out["2"]["z"]) <= 1e-12
