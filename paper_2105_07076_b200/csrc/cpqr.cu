@@ -25,6 +25,14 @@
 //   3. publishes (local max, lowest qualifying position, column id); after
 //      the barrier all CTAs reduce the G records identically.  When two CTAs'
 //      maxima differ by < 1e-14 relative, a second exact pass decides the tie.
+// Trailing update, organised for HBM bandwidth (the matrix does not fit on chip here):
+//   * long columns (>= kCoopRows active rows): half a block (16 warps) streams one column
+//     at a time -- the dot pass reads it from HBM with kUnroll independent loads per thread,
+//     the axpy pass re-reads it from L2 (148 x 2 columns in flight fit) and writes it back,
+//     so a step costs two HBM accesses per element instead of three; the two halves of a
+//     block work on different columns, so one half's reduction barrier overlaps the other's
+//     streaming;
+//   * short columns: a warp per column, loads unrolled the same way.
 // The owner of pivot s writes beta and the scaled reflector tail back into
 // the pivot column at the start of step s+1, so W ends up holding exactly the
 // reference's `work` matrix (R above the diagonal, reflectors below).
@@ -58,7 +66,9 @@ struct CpqrArgs {
     int64_t ldx;
 };
 
-constexpr int kCpqrThreads = 256;
+constexpr int kCpqrThreads = 1024;  // 32 warps per SM: enough loads in flight to stream HBM
+constexpr int kUnroll = 8;           // independent 8-byte loads per thread and loop trip
+constexpr int kCoopRows = 2048;      // columns at least this long are streamed by half a block each
 constexpr double kTieFactor = 1.0 - 1e-14;  // qr.cpp:71
 constexpr double kRecompute = 1e-6;          // qr.cpp:100
 
@@ -98,6 +108,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
     long long* s_pos = reinterpret_cast<long long*>(s_anchor + nc);  // nc
 
     __shared__ double red_d[32];
+    __shared__ double red_h[64];    // the two half-block reductions of the trailing update
     __shared__ long long red_l[32];
     __shared__ double s_scalar[3];  // tau, beta, scale
     __shared__ long long s_sel[2];  // pivot column, its position before the swap
@@ -295,71 +306,129 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
         __syncthreads();
 
         // (2) trailing update + norm downdate (qr.cpp:93-106).
-        if (coop) {  // one column at a time, rows over the whole block
-            for (int lc = 0; lc < myn; ++lc) {
-                if (s_pos[lc] <= s) continue;  // uniform across the block
+        if (coop || len >= kCoopRows) {
+            // half a block per column; rows split over the half's 16 warps
+            const int H = blockDim.x >> 1, half = tid / H, ht = tid - half * H;
+            const int hw = ht >> 5, hnw = H >> 5;
+            double* hred = red_h + half * 32;
+            auto half_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(H) : "memory"); };
+            auto half_sum = [&](double v) -> double {
+                v = warp_sum(v);
+                half_sync();  // the scratch of the previous reduction has been read
+                if (lane == 0) hred[hw] = v;
+                half_sync();
+                double t = lane < hnw ? hred[lane] : 0.0;
+                return warp_sum(t);
+            };
+            for (int lc = half; lc < myn; lc += 2) {
+                if (s_pos[lc] <= s) continue;  // uniform across the half
                 double* col = W + (c0 + lc) * ldw + s;
                 double head;
                 if (tau != 0.0) {
+                    double dd[kUnroll];
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) dd[u] = 0.0;
+                    for (int i0 = 1 + ht; i0 < len; i0 += H * kUnroll) {
+                        double yv[kUnroll];
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int i = i0 + u * H;
+                            yv[u] = i < len ? ld_cg(col + i) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int i = i0 + u * H;
+                            if (i < len) dd[u] += xv[i] * yv[u];
+                        }
+                    }
                     double d = 0.0;
-                    for (int i = 1 + tid; i < len; i += blockDim.x) d += xv[i] * ld_cg(col + i);
-                    d = block_sum(d, red_d);
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) d += dd[u];
+                    d = half_sum(d);
                     const double y0 = ld_cg(col);
                     const double w = mul_rn(add_rn(y0, d), tau);
                     head = sub_rn(y0, w);
-                    __syncthreads();  // every thread read y0 before it is overwritten
-                    if (tid == 0) st_cg(col, head);
-                    for (int i = 1 + tid; i < len; i += blockDim.x)
-                        st_cg(col + i, sub_rn(ld_cg(col + i), mul_rn(w, xv[i])));
+                    half_sync();  // every thread of the half read y0 before it is overwritten
+                    if (ht == 0) st_cg(col, head);
+                    for (int i0 = 1 + ht; i0 < len; i0 += H * kUnroll) {  // second pass: L2 hits
+                        double yv[kUnroll];
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int i = i0 + u * H;
+                            yv[u] = i < len ? ld_cg(col + i) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < kUnroll; ++u) {
+                            const int i = i0 + u * H;
+                            if (i < len) st_cg(col + i, sub_rn(yv[u], mul_rn(w, xv[i])));
+                        }
+                    }
                 } else {
                     head = ld_cg(col);
                 }
                 double lv = sub_rn(s_live[lc], mul_rn(head, head));
                 if (lv < 0.0) lv = 0.0;
                 if (lv <= mul_rn(kRecompute, s_anchor[lc])) {
-                    __syncthreads();  // the updated rows are visible block-wide
+                    half_sync();  // the updated rows are visible to the whole half
                     double f = 0.0;
-                    for (int i = 1 + tid; i < len; i += blockDim.x) {
+                    for (int i = 1 + ht; i < len; i += H) {
                         const double v = ld_cg(col + i);
                         f += v * v;
                     }
-                    f = block_sum(f, red_d);
+                    f = half_sum(f);
                     lv = f;
-                    if (tid == 0) s_anchor[lc] = f;
+                    if (ht == 0) s_anchor[lc] = f;
                 }
-                __syncthreads();
-                if (tid == 0) s_live[lc] = lv;
+                half_sync();  // s_live / s_anchor of this column have been read by every thread
+                if (ht == 0) s_live[lc] = lv;
             }
-        }
-        for (int lc = coop ? myn : warp; lc < myn; lc += nwarps) {
-            if (s_pos[lc] <= s) continue;
-            double* col = W + (c0 + lc) * ldw + s;
-            double head;
-            if (tau != 0.0) {
-                double d = 0.0;
-                for (int i = 1 + lane; i < len; i += 32) d += xv[i] * ld_cg(col + i);
-                d = warp_sum(d);
-                const double y0 = ld_cg(col);
-                const double w = mul_rn(add_rn(y0, d), tau);
-                head = sub_rn(y0, w);
-                if (lane == 0) st_cg(col, head);
-                for (int i = 1 + lane; i < len; i += 32) st_cg(col + i, sub_rn(ld_cg(col + i), mul_rn(w, xv[i])));
-            } else {
-                head = ld_cg(col);
-            }
-            double lv = sub_rn(s_live[lc], mul_rn(head, head));
-            if (lv < 0.0) lv = 0.0;
-            if (lv <= mul_rn(kRecompute, s_anchor[lc])) {
-                double f = 0.0;
-                for (int i = 1 + lane; i < len; i += 32) {
-                    const double v = ld_cg(col + i);
-                    f += v * v;
+        } else {
+            for (int lc = warp; lc < myn; lc += nwarps) {
+                if (s_pos[lc] <= s) continue;
+                double* col = W + (c0 + lc) * ldw + s;
+                double head;
+                if (tau != 0.0) {
+                    double dd[4] = {0.0, 0.0, 0.0, 0.0};
+                    for (int i0 = 1 + lane; i0 < len; i0 += 128) {
+                        double yv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) yv[u] = i0 + 32 * u < len ? ld_cg(col + i0 + 32 * u) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i0 + 32 * u < len) dd[u] += xv[i0 + 32 * u] * yv[u];
+                    }
+                    const double d = warp_sum((dd[0] + dd[1]) + (dd[2] + dd[3]));
+                    const double y0 = ld_cg(col);
+                    const double w = mul_rn(add_rn(y0, d), tau);
+                    head = sub_rn(y0, w);
+                    __syncwarp();  // every lane read y0 before it is overwritten
+                    if (lane == 0) st_cg(col, head);
+                    for (int i0 = 1 + lane; i0 < len; i0 += 128) {
+                        double yv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) yv[u] = i0 + 32 * u < len ? ld_cg(col + i0 + 32 * u) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (i0 + 32 * u < len) st_cg(col + i0 + 32 * u, sub_rn(yv[u], mul_rn(w, xv[i0 + 32 * u])));
+                    }
+                } else {
+                    head = ld_cg(col);
                 }
-                f = warp_sum(f);
-                lv = f;
-                if (lane == 0) s_anchor[lc] = f;
+                double lv = sub_rn(s_live[lc], mul_rn(head, head));
+                if (lv < 0.0) lv = 0.0;
+                if (lv <= mul_rn(kRecompute, s_anchor[lc])) {
+                    __syncwarp();
+                    double f = 0.0;
+                    for (int i = 1 + lane; i < len; i += 32) {
+                        const double v = ld_cg(col + i);
+                        f += v * v;
+                    }
+                    f = warp_sum(f);
+                    lv = f;
+                    if (lane == 0) s_anchor[lc] = f;
+                }
+                if (lane == 0) s_live[lc] = lv;
             }
-            if (lane == 0) s_live[lc] = lv;
         }
         __syncthreads();
         prev_piv = piv;
