@@ -229,7 +229,7 @@ cudaError_t run_cpqr(idk_context* h, const CpqrChoice& ch, double* W, int64_t mr
                                          Win, ldin);
     return idk::cpqr_launch(W, ldw, static_cast<int>(mrows), n, static_cast<int>(k), pos, piv, taus, base + w.pub,
                             reinterpret_cast<unsigned*>(base + w.barrier), h->num_sms, cpqr_ctas(h), h->stream,
-                            w.has_xg ? reinterpret_cast<double*>(base + w.xg) : nullptr);
+                            w.has_xg ? reinterpret_cast<double*>(base + w.xg) : nullptr, Win, ldin);
 }
 
 // CPQR(W) -> Z, C, cols; W is m' x n (ld m'), already resident and mutable.
@@ -286,14 +286,12 @@ int det_id(idk_context* h, const double* d_a, int64_t m, int64_t n, int64_t lda,
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     double* W = reinterpret_cast<double*>(h->ws + wofs);
     mark(h, 0);
-    // the resident CPQR reads A itself once and writes the factor to W: no working copy
-    const bool direct = !trans && ch.resident;
+    // both CPQR kernels read A itself once and write the factor / the working copy to W
+    // (the streaming kernel during its norm pass): no separate copy of A
+    const bool direct = !trans;
     if (trans) {
         IDK_CUDA(idk::transpose_copy(d_a, lda, n, m, W, m, h->stream));
         h->launches += 1;
-    } else if (!direct) {
-        IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
-                                   cudaMemcpyDeviceToDevice, h->stream));
     }
     mark(h, 1);
     return factor_and_solve(h, ch, W, m, n, k, h->ws, w, d_a, lda, m, trans, d_cols, d_z, d_c, true,
@@ -925,13 +923,11 @@ int idk_qr_column_pivoted(idk_handle h, const double* d_a, int64_t m, int64_t n,
     if ((rc = ensure(h, &h->ws, &h->ws_cap, cv.total))) return rc;
     char* base = h->ws;
     double* W = reinterpret_cast<double*>(base + wofs);
-    if (!ch.resident)  // the streaming kernel factors in place; the resident one reads A directly
-        IDK_CUDA(cudaMemcpy2DAsync(W, sizeof(double) * m, d_a, sizeof(double) * lda, sizeof(double) * m, n,
-                                   cudaMemcpyDeviceToDevice, h->stream));
+    // both CPQR kernels read A directly (the streaming one writes its working copy during the norm pass)
     long long* pos = reinterpret_cast<long long*>(base + w.pos);
     long long* piv = reinterpret_cast<long long*>(base + w.pivots);
     double* taus = reinterpret_cast<double*>(base + w.taus);
-    IDK_CUDA(run_cpqr(h, ch, W, m, n, steps, base, w, m, ch.resident ? d_a : nullptr, lda));
+    IDK_CUDA(run_cpqr(h, ch, W, m, n, steps, base, w, m, d_a, lda));
     long long* perm = d_perm ? reinterpret_cast<long long*>(d_perm) : reinterpret_cast<long long*>(base + permofs);
     IDK_CUDA(idk::cpqr_finish(W, m, static_cast<int>(m), n, static_cast<int>(steps), pos, piv, taus, perm, d_r, d_q,
                               h->stream));

@@ -64,6 +64,8 @@ struct CpqrArgs {
     unsigned* barrier;    // zeroed before launch
     double* xglobal;      // per-CTA reflector buffers (G x ldx) when m doubles do not fit in shared memory
     int64_t ldx;
+    const double* Win;    // the matrix as the caller holds it (read once: norms + working copy into W), or W
+    int64_t ldin;
 };
 
 constexpr int kCpqrThreads = 1024;  // 32 warps per SM: enough loads in flight to stream HBM
@@ -125,13 +127,18 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
     // Few columns per CTA (tall matrices): every warp of the CTA works on one
     // column at a time (rows split over the whole block) instead of a warp per column.
     const bool coop = myn < nwarps;
-    // ---- initial squared norms (qr.cpp:56-62) ----
+    // ---- initial squared norms (qr.cpp:56-62); the same pass writes the working copy when the
+    // caller's matrix is read in place (no separate copy of A before the factorisation) ----
+    const bool copy_in = a.Win != W;
     if (coop) {
         for (int lc = 0; lc < myn; ++lc) {
-            const double* col = W + (c0 + lc) * ldw;
+            const double* src = a.Win + (c0 + lc) * a.ldin;
+            double* dst = W + (c0 + lc) * ldw;
             double s = 0.0;
+#pragma unroll 4
             for (int i = tid; i < m; i += blockDim.x) {
-                const double v = ld_cg(col + i);
+                const double v = ld_cg(src + i);
+                if (copy_in) st_cg(dst + i, v);
                 s += v * v;
             }
             s = block_sum(s, red_d);
@@ -143,13 +150,20 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
         }
     }
     for (int lc = coop ? myn : warp; lc < myn; lc += nwarps) {
-        const double* col = W + (c0 + lc) * ldw;
-        double s = 0.0;
-        for (int i = lane; i < m; i += 32) {
-            const double v = ld_cg(col + i);
-            s += v * v;
+        const double* src = a.Win + (c0 + lc) * a.ldin;
+        double* dst = W + (c0 + lc) * ldw;
+        double ss[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int i0 = lane; i0 < m; i0 += 128) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = i0 + 32 * u < m ? ld_cg(src + i0 + 32 * u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (copy_in && i0 + 32 * u < m) st_cg(dst + i0 + 32 * u, v[u]);
+                ss[u] += v[u] * v[u];
+            }
         }
-        s = warp_sum(s);
+        const double s = warp_sum((ss[0] + ss[1]) + (ss[2] + ss[3]));
         if (lane == 0) {
             s_live[lc] = s;
             s_anchor[lc] = s;
@@ -510,7 +524,7 @@ int64_t cpqr_xglobal_ld(int m) { return (static_cast<int64_t>(m) + 31) & ~31LL; 
 // Host launcher.  `ws_pub` must hold 3*G CpqrPub, `barrier` one unsigned.
 cudaError_t cpqr_launch(double* W, int64_t ldw, int m, int64_t n, int k, long long* pos_out,
                         long long* pivots, double* taus, void* ws_pub, unsigned* barrier, int num_sms,
-                        int max_ctas, cudaStream_t stream, double* xglobal) {
+                        int max_ctas, cudaStream_t stream, double* xglobal, const double* Win, int64_t ldin) {
     // Block-distribute columns: G CTAs, each at most one per SM (co-residency).
     int64_t G = std::min<int64_t>(n, static_cast<int64_t>(max_ctas > 0 ? max_ctas : num_sms));
     int cols = static_cast<int>((n + G - 1) / G);
@@ -538,6 +552,8 @@ cudaError_t cpqr_launch(double* W, int64_t ldw, int m, int64_t n, int k, long lo
     args.barrier = barrier;
     args.xglobal = xg ? xglobal : nullptr;
     args.ldx = cpqr_xglobal_ld(m);
+    args.Win = Win ? Win : W;
+    args.ldin = Win ? ldin : ldw;
     void* params[] = {&args};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_persistent_kernel), dim3(static_cast<unsigned>(G)),
                                        dim3(kCpqrThreads), params, smem, stream);

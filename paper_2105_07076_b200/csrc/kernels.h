@@ -51,7 +51,8 @@ constexpr size_t kCpqrPubBytes = 32;
 size_t cpqr_smem_bytes(int m, int cols_per_cta);
 cudaError_t cpqr_launch(double* W, int64_t ldw, int m, int64_t n, int k, long long* pos_out, long long* pivots,
                         double* taus, void* ws_pub, unsigned* barrier, int num_sms, int max_ctas,
-                        cudaStream_t stream, double* xglobal = nullptr);
+                        cudaStream_t stream, double* xglobal = nullptr, const double* Win = nullptr,
+                        int64_t ldin = 0);  // Win: read A in place, the working copy W is written by the norm pass
 int64_t cpqr_xglobal_ld(int m);
 cudaError_t cpqr_finish(const double* W, int64_t ldw, int m, int64_t n, int k, const long long* pos,
                         const long long* pivots, const double* taus, long long* perm, double* R, double* Q,
