@@ -175,7 +175,7 @@ CpqrChoice choose_cpqr(idk_context* h, int64_t mrows, int64_t n, int64_t k) {
 // Work buffers of one CPQR + Z solve on an m' x n matrix.
 struct CpqrWs {
     size_t pos, pivots, taus, pub, barrier, r11, status;
-    size_t xg = 0;  // streaming CPQR of a tall matrix: per-CTA reflector buffers in L2
+    size_t xg = 0;  // streaming CPQR of a tall matrix: the shared, double-buffered reflector in L2
     bool has_xg = false;
 };
 
@@ -191,8 +191,7 @@ CpqrWs carve_cpqr(Carve& cv, int64_t mrows, int64_t n, int64_t k, int num_sms, c
     CpqrWs w;
     if (!ch.resident && cpqr_needs_xglobal(mrows, n, num_sms)) {
         w.has_xg = true;
-        w.xg = cv.take(sizeof(double) * static_cast<size_t>(std::min<int64_t>(n, num_sms)) *
-                       static_cast<size_t>(idk::cpqr_xglobal_ld(static_cast<int>(mrows))));
+        w.xg = cv.take(sizeof(double) * 2 * static_cast<size_t>(idk::cpqr_xglobal_ld(static_cast<int>(mrows))));
     }
     w.pos = cv.take(sizeof(long long) * n);
     w.pivots = cv.take(sizeof(long long) * k);

@@ -104,7 +104,12 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
     const int nc = a.cols_per_cta;
     // m doubles: pivot column -> reflector; in shared memory, or for tall
     // matrices (m > ~24k rows) this CTA's own L2-resident buffer
-    double* xv = a.xglobal ? a.xglobal + static_cast<int64_t>(blockIdx.x) * a.ldx : sm;
+    // The reflector: in shared memory, or -- when m doubles do not fit -- ONE L2-resident copy
+    // shared by all CTAs, double-buffered by step parity.  Every CTA builds the same values
+    // and writes them (identical bits), and reads them only after its own writes, so the
+    // copy needs no extra grid barrier; 148 private copies would take 148 x 8m bytes of the
+    // L2 that the columns in flight need.
+    double* xv = a.xglobal ? a.xglobal : sm;
     double* s_live = a.xglobal ? sm : xv + ((m + 1) & ~1);  // nc
     double* s_anchor = s_live + nc;        // nc
     long long* s_pos = reinterpret_cast<long long*>(s_anchor + nc);  // nc
@@ -275,23 +280,27 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
     for (int s = 0; s < a.k; ++s) {
         const long long piv = s_sel[0], ppos = s_sel[1];
         const int len = m - s;
+        const double* xvp = xv;  // the previous step's reflector
+        if (a.xglobal) xv = a.xglobal + (s & 1) * a.ldx;
 
         // (0) write back the previous reflector into its column (owner only).
         if (prev_piv >= 0 && prev_piv >= c0 && prev_piv < c0 + myn) {
             double* col = W + prev_piv * ldw + (s - 1);
-            for (int i = tid; i < len + 1; i += blockDim.x) __stcg(col + i, i == 0 ? s_scalar[1] : xv[i]);
+            for (int i = tid; i < len + 1; i += blockDim.x) __stcg(col + i, i == 0 ? s_scalar[1] : xvp[i]);
         }
         __syncthreads();
 
-        // (1) pivot column -> reflector (qr.cpp:16-28).
+        // (1) pivot column -> reflector (qr.cpp:16-28).  The buffer is written once, with the
+        // final values (a shared L2 copy is written by every CTA: no read-modify-write).
         const double* pcol = W + piv * ldw + s;
-        for (int i = tid; i < len; i += blockDim.x) xv[i] = ld_cg(pcol + i);
-        __syncthreads();
         double t = 0.0;
-        for (int i = 1 + tid; i < len; i += blockDim.x) t += xv[i] * xv[i];
+        for (int i = 1 + tid; i < len; i += blockDim.x) {
+            const double v = ld_cg(pcol + i);
+            t += v * v;
+        }
         const double tail = block_sum(t, red_d);
         if (tid == 0) {
-            const double alpha = xv[0];
+            const double alpha = ld_cg(pcol);
             double tau = 0.0, beta = alpha, scale = 1.0;
             if (len > 1 && tail != 0.0) {
                 beta = -copysign(sqrt(add_rn(mul_rn(alpha, alpha), tail)), alpha);
@@ -308,9 +317,12 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
         }
         __syncthreads();
         const double tau = s_scalar[0];
-        if (tau != 0.0) {
+        {
             const double scale = s_scalar[2];
-            for (int i = 1 + tid; i < len; i += blockDim.x) xv[i] = mul_rn(xv[i], scale);
+            for (int i = tid; i < len; i += blockDim.x) {
+                const double v = ld_cg(pcol + i);
+                xv[i] = (tau != 0.0 && i > 0) ? mul_rn(v, scale) : v;
+            }
         }
         // Replay the swap on positions (qr.cpp:79-86).
         for (int lc = tid; lc < myn; lc += blockDim.x) {
@@ -321,8 +333,11 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
 
         // (2) trailing update + norm downdate (qr.cpp:93-106).
         if (coop || len >= kCoopRows) {
-            // half a block per column; rows split over the half's 16 warps
-            const int H = blockDim.x >> 1, half = tid / H, ht = tid - half * H;
+            // half a block per column, rows split over the half's 16 warps; the whole block per
+            // column once two columns per SM no longer stay in L2 between their two passes
+            // (2 x G columns x len x 8 bytes against ~48 MB of the 126 MB L2)
+            const int P = (static_cast<double>(len) * 16.0 * G > 48e6) ? 1 : 2;
+            const int H = blockDim.x / P, half = tid / H, ht = tid - half * H;
             const int hw = ht >> 5, hnw = H >> 5;
             double* hred = red_h + half * 32;
             auto half_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "r"(H) : "memory"); };
@@ -334,7 +349,7 @@ __global__ void __launch_bounds__(kCpqrThreads) cpqr_persistent_kernel(CpqrArgs 
                 double t = lane < hnw ? hred[lane] : 0.0;
                 return warp_sum(t);
             };
-            for (int lc = half; lc < myn; lc += 2) {
+            for (int lc = half; lc < myn; lc += P) {
                 if (s_pos[lc] <= s) continue;  // uniform across the half
                 double* col = W + (c0 + lc) * ldw + s;
                 double head;
@@ -517,8 +532,8 @@ size_t cpqr_smem_bytes(int m, int cols_per_cta) {
 }
 
 // The reflector buffer moves to global memory (L2) when m doubles plus the
-// per-column state exceed the shared-memory budget; `xglobal` then needs G x
-// cpqr_xglobal_ld(m) doubles.
+// per-column state exceed the shared-memory budget; `xglobal` then needs
+// 2 * cpqr_xglobal_ld(m) doubles (one copy shared by all CTAs, double-buffered).
 int64_t cpqr_xglobal_ld(int m) { return (static_cast<int64_t>(m) + 31) & ~31LL; }
 
 // Host launcher.  `ws_pub` must hold 3*G CpqrPub, `barrier` one unsigned.
