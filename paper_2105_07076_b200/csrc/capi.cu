@@ -180,7 +180,7 @@ struct CpqrWs {
 };
 
 // The streaming kernel keeps the reflector (m doubles) in shared memory when
-// it fits; taller matrices keep one L2-resident copy per CTA instead.
+// it fits; taller matrices keep one L2-resident copy (double-buffered) shared by all CTAs.
 bool cpqr_needs_xglobal(int64_t mrows, int64_t n, int num_sms) {
     const int64_t G = std::min<int64_t>(n, num_sms);
     const int cols = static_cast<int>((n + G - 1) / G);

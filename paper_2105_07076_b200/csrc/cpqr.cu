@@ -62,7 +62,7 @@ struct CpqrArgs {
     CpqrPub* pub;         // 2 * G (double-buffered by step parity)
     CpqrPub* pub2;        // G (exact tie pass)
     unsigned* barrier;    // zeroed before launch
-    double* xglobal;      // per-CTA reflector buffers (G x ldx) when m doubles do not fit in shared memory
+    double* xglobal;      // shared reflector (2 x ldx, by step parity) when m doubles do not fit in shared memory
     int64_t ldx;
     const double* Win;    // the matrix as the caller holds it (read once: norms + working copy into W), or W
     int64_t ldin;
