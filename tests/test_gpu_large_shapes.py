@@ -2,7 +2,7 @@
 shape; qr.cpp:42-46 validates only max_steps).  The resident CPQR cannot hold
 these, so the streaming kernel runs with the matrix in HBM and -- when m
 doubles no longer fit in shared memory (m > ~24k rows) -- its reflector in an
-L2-resident buffer per CTA.  Compared with the reference library itself."""
+L2-resident buffer shared by all CTAs.  Compared with the reference library itself."""
 import numpy as np
 import pytest
 
