@@ -65,3 +65,24 @@ def test_qr_column_pivoted_30000_x_30000(idk, ref):
     assert np.array_equal(f.perm.cpu().numpy(), rperm)
     assert rel(f.r.cpu().numpy(), rr) <= 1e-10
     assert rel(f.q.cpu().numpy(), rq) <= 1e-10
+
+
+def test_optim_id_5000_x_3000_half_block_streaming(idk, ref):
+    """120 MB: too large for the on-chip CPQR, columns long enough (>= 2048 rows) for the
+    streaming kernel's half-block-per-column path with the reflector in shared memory."""
+    rng = np.random.default_rng(7)
+    m, n, k = 5000, 3000, 24
+    a = rng.standard_normal((m, 40)) @ (rng.standard_normal((40, n)) * np.exp(-np.arange(n) / 300.0))
+    a = np.asfortranarray(a + 1e-4 * rng.standard_normal((m, n)))
+    ctx = idk.context(0)
+    assert ctx.cpqr_plan(m, n, k)["kind"] == "streaming"
+    r = idk.optim_id(_dev(a), k)
+    rcols, rz, _ = ref.optim_id(a, k)
+    assert np.array_equal(r.cols.cpu().numpy(), rcols)
+    assert rel(r.z.cpu().numpy(), rz) <= 1e-10
+    assert np.array_equal(r.c.cpu().numpy(), a[:, rcols])
+    f = idk.qr_column_pivoted(_dev(a), k)
+    rq, rr, rperm = ref.qr_column_pivoted(a, k)
+    assert np.array_equal(f.perm.cpu().numpy(), rperm)
+    assert rel(f.r.cpu().numpy(), rr) <= 1e-10
+    assert rel(f.q.cpu().numpy(), rq) <= 1e-10
