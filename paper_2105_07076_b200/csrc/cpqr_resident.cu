@@ -602,10 +602,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                 const double w0 = __shfl_sync(kFull, todo ? wpend : 0.0, wl0);  // 0: already current
                 if (lc == winlc) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int i = l0 + q + S * r;
-                        if (i >= first && i < m) xbuf[i] = yr[r];
-                    }
+                    for (int r = 0; r < R; ++r) xbuf[l0 + q + S * r] = yr[r];  // retired / padding rows too
                 }
                 if (lane == 0) s_help[kHelpWarps] = w0;
             }
@@ -703,10 +700,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                 const double ww = __shfl_sync(kFull, todo ? wpend : 0.0, wl0);  // 0: already current
                 if (lc == winlc) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int i = l0 + q + S * r;
-                        if (i >= first && i < m) xbuf[i] = yr[r];
-                    }
+                    for (int r = 0; r < R; ++r) xbuf[l0 + q + S * r] = yr[r];  // retired / padding rows too
                 }
                 __syncwarp();
                 trace_by(lane == 0, step, 8);
