@@ -1103,7 +1103,14 @@ cpqr_resident_kernel(ResidentArgs a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&s_mbar[0]));
             trace_by(lane == 0, step, 8);
+            // With one or two threads per column the staging above is a long serial run of one
+            // or two lanes on the winner's critical path: the other warps hold their axpy until
+            // the hand-off (named barrier 1; cfg5 CPQR 0.4185 -> 0.4121 ms).  With wider groups
+            // the staging is short and the barrier costs more than it gives (cfg4 +0.4 %).
+            if constexpr (S <= 2) asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
             mbar_wait(smem_u32(&s_mbar[1]), static_cast<unsigned>(parity));  // candidate rows consumed
+        } else {
+            if constexpr (S <= 2) asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
         }
         do_axpy();
         trace(step, 7);
