@@ -636,6 +636,9 @@ cpqr_resident_kernel(ResidentArgs a) {
             for (int h = 0; h < nh; ++h) tt += s_help[h];  // fixed order: every helper gets the same sum
             const double al = s_help[kHelpWarps + 1];
             trace_by(pubwarp && lane == 0, step, 9);
+            // the other warps may start their axpy now: the shared-memory-heavy part of the
+            // publish (raw copy, pending update, norm) is done (named barrier 1)
+            if (pubwarp) asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
             double tu, be, sc;
             reflector_warp(al, tt, m - first, tu, be, sc);
             trace_by(pubwarp && lane == 0, step, 10);
@@ -680,9 +683,6 @@ cpqr_resident_kernel(ResidentArgs a) {
                     bulk_push(mapa_u32(da, g), sa, bytes, mapa_u32(mb, g));
                 }
                 trace_by(lane == 0, step, 3);
-                // let the other warps go: their axpys contend for shared memory, so
-                // they wait until the candidate is out (named barrier 1)
-                asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
             } else {
                 asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
             }
@@ -725,6 +725,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                     al = __shfl_sync(kFull, al, 0);  // row `first` is lane 0's first row
                     tl = warp_sum(tl);
                     trace_by(lane == 0, step, 9);
+                    asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");  // see below
                     reflector_warp(al, tl, m - first, tu, be, sc);
                     trace_by(lane == 0, step, 10);
 #pragma unroll
@@ -755,6 +756,7 @@ cpqr_resident_kernel(ResidentArgs a) {
                     al = __shfl_sync(kFull, al, 0);
                     tl = warp_sum(tl);
                     trace_by(lane == 0, step, 9);
+                    asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
                     reflector_warp(al, tl, m - first, tu, be, sc);
                     trace_by(lane == 0, step, 10);
                     for (int i0 = first + lane; i0 < m; i0 += 32 * kPubRegs) {
@@ -798,9 +800,11 @@ cpqr_resident_kernel(ResidentArgs a) {
                 bulk_push(mapa_u32(da, g), sa, bytes, mapa_u32(mb, g));
             }
             trace_by(lane == 0, step, 3);
-            // let the other warps go: their axpys contend for shared memory, so
-            // they wait until the candidate is out (named barrier 1)
-            asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
+            // The other warps' axpys contend for shared memory, so they wait on named barrier 1
+            // -- but only until the shared-memory-heavy part of the publish (raw copy, pending
+            // update, norm) is done: the arrive sits right after the norm above, and here for a
+            // CTA without a candidate.
+            if (!have) asm volatile("bar.arrive 1, %0;" ::"r"(T) : "memory");
         } else {
             asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory");
         }
