@@ -33,7 +33,7 @@ cudaError_t sketch_gemm_tma(const double* A, int64_t lda, const double* B, int64
                             cudaStream_t stream);
 cudaError_t omega_philox_group(double* out, int64_t l, int64_t m, const GroupSeeds& seeds, int count,
                                cudaStream_t stream);
-int sketch_gemm_pick_wm(int M);
+int sketch_gemm_pick_wm(int M, int64_t K = (1LL << 40));
 int sketch_gemm_pick_splits(int M, int64_t N, int64_t K, int num_sms);
 cudaError_t sketch_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, bool b_trans, double* Y,
                         int64_t ldc, int M, int64_t N, int64_t K, int splits, double* partial, cudaStream_t stream);
